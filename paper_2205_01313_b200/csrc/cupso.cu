@@ -1,0 +1,1060 @@
+// cupso.cu -- host engine and C-ABI of libcupso.so (see include/cupso.h).
+//
+// The host side owns a device-resident swarm (axis-major SoA, rows padded to
+// a multiple of 64 particles so every row is 512-byte aligned and the
+// two-particle double2 path never straddles a row), a small control block
+// (gbest snapshot/live records, trace arrays, counters) and a stream. A
+// "step" launches one of the six aggregation variants for a range of
+// iterations and times exactly that range with CUDA events.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/cupso.h"
+#include "cupso_kernels.cuh"
+
+using namespace cupso;
+
+namespace {
+
+thread_local std::string g_err;
+
+cupso_status fail(cupso_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(CUPSO_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define TRY(call)                        \
+  do {                                   \
+    cupso_status s_ = (call);            \
+    if (s_ != CUPSO_OK) return s_;       \
+  } while (0)
+
+// fitness.hpp:87-95 registry order, plus the harness Rastrigin.
+const char* const kFitNames[] = {"cubic", "sphere", "rosenbrock", "griewank", "rastrigin"};
+const double kFitLo[] = {-100.0, -100.0, -2.048, -600.0, -5.12};
+const double kFitHi[] = {100.0, 100.0, 2.048, 600.0, 5.12};
+constexpr int kNumFit = 5;
+
+const char* const kVarNames[] = {"cuda-reduction", "cuda-unrolled", "cuda-queue",
+                                 "cuda-queue-lock", "cuda-sync",    "cuda-async"};
+constexpr int kNumVar = 6;
+
+// std::to_string(double) == "%f" (params.hpp:38-42 message text)
+std::string fstr(double v) {
+  char b[64];
+  snprintf(b, sizeof b, "%f", v);
+  return b;
+}
+
+cupso_status validate(const cupso_params* p) {
+  if (!p) return fail(CUPSO_EINVAL, "pso_params: null");
+  if (!(p->min_pos < p->max_pos))
+    return fail(CUPSO_EINVAL, "pso_params: min_pos (%s) must be < max_pos (%s)",
+                fstr(p->min_pos).c_str(), fstr(p->max_pos).c_str());
+  if (!(p->min_v <= p->max_v))
+    return fail(CUPSO_EINVAL, "pso_params: min_v (%s) must be <= max_v (%s)",
+                fstr(p->min_v).c_str(), fstr(p->max_v).c_str());
+  if (p->particle_cnt < 1) return fail(CUPSO_EINVAL, "pso_params: particle_cnt must be >= 1");
+  if (p->dims < 1) return fail(CUPSO_EINVAL, "pso_params: dims must be >= 1");
+  if (p->max_iter < 1) return fail(CUPSO_EINVAL, "pso_params: max_iter must be >= 1");
+  if (p->group_size < 1) return fail(CUPSO_EINVAL, "pso_params: group_size must be >= 1");
+  return CUPSO_OK;
+}
+
+uint32_t bit_ceil(uint32_t v) {
+  uint32_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// ---------------------------------------------------------- NCCL (dlopen)
+// Loaded lazily so the library has no link-time NCCL dependency and shares
+// whatever libnccl.so.2 the process (e.g. torch) already mapped.
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, const void*, int) = nullptr;  // ncclUniqueId by value (128 B)
+  int (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+  bool ok = false;
+};
+struct NcclUid {
+  char internal[128];
+};
+using CommInitRankFn = int (*)(void**, int, NcclUid, int);
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!a.h) a.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!a.h) return a;
+    a.getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(a.h, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<int (*)(void**, int, const void*, int)>(dlsym(a.h, "ncclCommInitRank"));
+    a.allGather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+        dlsym(a.h, "ncclAllGather"));
+    a.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(a.h, "ncclCommDestroy"));
+    a.getErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(a.h, "ncclGetErrorString"));
+    a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.commDestroy;
+    return a;
+  }();
+  return api;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ swarm
+struct cupso_swarm {
+  int device = 0;
+  int fid = 0;
+  uint64_t seed = 0;
+  cupso_params gp{};          // global params (shards: the whole swarm)
+  KParams P{};
+  KState S{};
+  KCtl C{};
+  uint32_t T = 0;             // trace capacity = max_iter
+  uint32_t t = 0;             // iterations completed
+  bool initialized = false;
+  double initial_fit = -INFINITY;
+  uint32_t initial_particle = kNoParticle;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<void*> allocs;
+  unsigned char* ctl_block = nullptr;   // records + counters
+  size_t rec_bytes = 0;
+  double* eval_buf = nullptr;           // fitness export scratch
+  uint32_t groups = 0;
+  int sync_grid = 0;
+  uint32_t q_alloc = 0;
+  std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
+  std::vector<uint8_t> is_async;
+  std::map<std::tuple<int, uint32_t, uint32_t>, cudaGraphExec_t> graphs;
+  // multi-GPU exchange
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+  unsigned char* rec_local = nullptr;   // [rec_bytes]
+  unsigned char* rec_all = nullptr;     // [nranks * rec_bytes]
+};
+
+namespace {
+
+cupso_status dmalloc(cupso_swarm* h, void** p, size_t bytes) {
+  CK(cudaMalloc(p, bytes));
+  h->allocs.push_back(*p);
+  return CUPSO_OK;
+}
+
+template <typename Fn>
+cupso_status dispatch_fit(int fid, Fn&& fn) {
+  switch (fid) {
+    case kCubic: fn(std::integral_constant<int, kCubic>{}); break;
+    case kSphere: fn(std::integral_constant<int, kSphere>{}); break;
+    case kRosenbrock: fn(std::integral_constant<int, kRosenbrock>{}); break;
+    case kGriewank: fn(std::integral_constant<int, kGriewank>{}); break;
+    case kRastrigin: fn(std::integral_constant<int, kRastrigin>{}); break;
+    default: return fail(CUPSO_EINVAL, "unknown fitness id %d", fid);
+  }
+  return CUPSO_OK;
+}
+
+void key_schedule(uint64_t seed, KParams& P) {
+  uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    P.k0[r] = k0;
+    P.k1[r] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+int num_sms(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v > 0 ? v : 1;
+}
+
+size_t sync_smem(const cupso_swarm* h) { return static_cast<size_t>(h->P.d) * sizeof(double); }
+constexpr uint32_t kMaxSyncDims = 12288;  // 96 KiB of dynamic smem for the gbest snapshot
+
+// Persistent grid: every block co-resident (required by the grid barrier).
+cupso_status ensure_sync_grid(cupso_swarm* h) {
+  if (h->sync_grid > 0) return CUPSO_OK;
+  if (h->P.d > kMaxSyncDims)
+    return fail(CUPSO_EINVAL, "cuda-sync/async: dims (%u) above %u", h->P.d, kMaxSyncDims);
+  const size_t smem = sync_smem(h);
+  int per_sm = 0;
+  cudaError_t e = cudaSuccess;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(k_sync<f>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_async<f>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_propose<f>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    int a = 0, b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sync<f>, kSyncThreads, smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_async<f>, kSyncThreads, smem);
+    per_sm = std::min(a, b);
+  });
+  CK(e);
+  if (per_sm < 1) return fail(CUPSO_ECUDA, "cuda-sync: kernel cannot be resident (occupancy 0)");
+  const uint64_t pairs = (h->P.n + 1ull) / 2;
+  uint64_t grid = static_cast<uint64_t>(per_sm) * num_sms(h->device);
+  // keep at least ~2 pairs per thread of work per block when the swarm is small
+  const uint64_t min_work = std::max<uint64_t>(1, pairs / (2 * kSyncThreads));
+  grid = std::max<uint64_t>(1, std::min(grid, min_work));
+  h->sync_grid = static_cast<int>(grid);
+  if (h->q_alloc < grid) {
+    void *qf, *qi, *qp;
+    TRY(dmalloc(h, &qf, 3 * grid * sizeof(double)));
+    TRY(dmalloc(h, &qi, 3 * grid * sizeof(uint32_t)));
+    TRY(dmalloc(h, &qp, 3 * grid * h->P.d * sizeof(double)));
+    h->C.q_fit = static_cast<double*>(qf);
+    h->C.q_idx = static_cast<uint32_t*>(qi);
+    h->C.q_pos = static_cast<double*>(qp);
+    h->C.q_cap = static_cast<uint32_t>(grid);
+    h->q_alloc = static_cast<uint32_t>(grid);
+  }
+  return CUPSO_OK;
+}
+
+cupso_status copy_record(cupso_swarm* h, Rec* dst, const Rec* src) {
+  CK(cudaMemcpyAsync(dst, src, h->rec_bytes, cudaMemcpyDeviceToDevice, h->stream));
+  return CUPSO_OK;
+}
+
+// Classic variants: capture [t0, t0+iters) as one CUDA graph (2 or 1 launches per iteration).
+cupso_status classic_graph(cupso_swarm* h, int variant, uint32_t t0, uint32_t iters,
+                           cudaGraphExec_t* out) {
+  const auto key = std::make_tuple(variant, t0, iters);
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) {
+    *out = it->second;
+    return CUPSO_OK;
+  }
+  const uint32_t gs = h->P.gs;
+  if (gs > 1024)
+    return fail(CUPSO_EINVAL, "%s: group_size (%u) must be <= 1024 (CUDA block limit)",
+                kVarNames[variant], gs);
+  const uint32_t padded = bit_ceil(gs);
+  const size_t smem = padded * (sizeof(double) + sizeof(uint32_t));
+  const uint32_t groups = h->groups;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t le = cudaSuccess;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    for (uint32_t t = t0; t < t0 + iters && le == cudaSuccess; ++t) {
+      switch (variant) {
+        case CUPSO_REDUCTION:
+          k_classic_step<f, kTree><<<groups, gs, smem, h->stream>>>(h->P, h->S, h->C, t, padded);
+          k_classic_fold<kTree><<<1, gs, smem, h->stream>>>(h->P, h->S, h->C, t, groups, padded);
+          break;
+        case CUPSO_UNROLLED:
+          k_classic_step<f, kTreeUnrolled><<<groups, gs, smem, h->stream>>>(h->P, h->S, h->C, t, padded);
+          k_classic_fold<kTreeUnrolled><<<1, gs, smem, h->stream>>>(h->P, h->S, h->C, t, groups, padded);
+          break;
+        case CUPSO_QUEUE:
+          k_classic_step<f, kQueue><<<groups, gs, smem, h->stream>>>(h->P, h->S, h->C, t, padded);
+          k_classic_fold<kQueue><<<1, gs, smem, h->stream>>>(h->P, h->S, h->C, t, groups, padded);
+          break;
+        case CUPSO_QUEUE_LOCK:
+          k_classic_step<f, kQueueLock><<<groups, gs, smem, h->stream>>>(h->P, h->S, h->C, t, padded);
+          break;
+      }
+      le = cudaGetLastError();
+    }
+  });
+  cudaError_t ee = cudaStreamEndCapture(h->stream, &g);
+  CK(le);
+  CK(ee);
+  cudaGraphExec_t ge;
+  cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  CK(ie);
+  h->graphs[key] = ge;
+  *out = ge;
+  return CUPSO_OK;
+}
+
+cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_t t1) {
+  TRY(ensure_sync_grid(h));
+  const size_t smem = sync_smem(h);
+  cudaError_t e = cudaSuccess;
+  // counters: bar (sync), seq (async), q_count[3]
+  CK(cudaMemsetAsync(h->C.bar, 0, sizeof(uint32_t), h->stream));
+  CK(cudaMemsetAsync(h->C.seq, 0, sizeof(uint32_t), h->stream));
+  CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    void* args[] = {&h->P, &h->S, &h->C, &t0, &t1};
+    if (variant == CUPSO_SYNC)
+      e = cudaLaunchCooperativeKernel((void*)k_sync<f>, dim3(h->sync_grid), dim3(kSyncThreads), args,
+                                      smem, h->stream);
+    else
+      e = cudaLaunchCooperativeKernel((void*)k_async<f>, dim3(h->sync_grid), dim3(kSyncThreads), args,
+                                      smem, h->stream);
+  });
+  CK(e);
+  return CUPSO_OK;
+}
+
+cupso_status propose_launch(cupso_swarm* h, uint32_t t, unsigned char* record_dev) {
+  TRY(ensure_sync_grid(h));
+  const size_t smem = sync_smem(h);
+  cudaError_t e = cudaSuccess;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    k_propose<f><<<h->sync_grid, kSyncThreads, smem, h->stream>>>(h->P, h->S, h->C, t, record_dev);
+    e = cudaGetLastError();
+  });
+  CK(e);
+  return CUPSO_OK;
+}
+
+cupso_status commit_launch(cupso_swarm* h, uint32_t t, const unsigned char* recs, uint32_t n) {
+  k_commit<<<1, 256, 0, h->stream>>>(h->P, h->C, t, recs, n, h->rec_bytes, 1);
+  CK(cudaGetLastError());
+  return CUPSO_OK;
+}
+
+// NCCL-backed sharded sync step: propose -> allgather -> commit per iteration.
+cupso_status sharded_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
+  NcclApi& api = nccl();
+  for (uint32_t t = t0; t < t1; ++t) {
+    TRY(propose_launch(h, t, h->rec_local));
+    const int r = api.allGather(h->rec_local, h->rec_all, h->rec_bytes, /*ncclInt8*/ 0, h->comm,
+                                h->stream);
+    if (r != 0)
+      return fail(CUPSO_ERUNTIME, "ncclAllGather failed: %s",
+                  api.getErrorString ? api.getErrorString(r) : "?");
+    TRY(commit_launch(h, t, h->rec_all, static_cast<uint32_t>(h->nranks)));
+  }
+  return CUPSO_OK;
+}
+
+cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* seconds) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  if (variant < 0 || variant >= kNumVar) return fail(CUPSO_EINVAL, "unknown variant %d", variant);
+  if (!h->initialized) return fail(CUPSO_ELOGIC, "cupso_step before cupso_init");
+  if (static_cast<uint64_t>(h->t) + iters > h->T)
+    return fail(CUPSO_EINVAL, "cupso_step: %u + %u iterations exceed max_iter (%u)", h->t, iters, h->T);
+  if (h->nranks > 1 && variant != CUPSO_SYNC)
+    return fail(CUPSO_EINVAL, "sharded swarms step with cuda-sync only");
+  CK(cudaSetDevice(h->device));
+  const uint32_t t0 = h->t, t1 = h->t + iters;
+  cudaGraphExec_t ge = nullptr;
+  if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
+  if (iters && variant == CUPSO_QUEUE_LOCK) TRY(copy_record(h, h->C.live, h->C.snap));
+  if (iters && variant == CUPSO_ASYNC) {
+    TRY(copy_record(h, h->C.live, h->C.snap));
+    CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
+  }
+  if (iters && (variant == CUPSO_SYNC || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
+  CK(cudaEventRecord(h->ev0, h->stream));
+  if (iters) {
+    if (ge) {
+      CK(cudaGraphLaunch(ge, h->stream));
+    } else if (variant == CUPSO_SYNC && h->comm) {
+      TRY(sharded_steps(h, t0, t1));
+    } else {
+      constexpr uint32_t kChunk = 1u << 20;  // keeps the barrier counter far from wrap
+      for (uint32_t a = t0; a < t1; a += std::min(kChunk, t1 - a))
+        TRY(launch_persistent(h, variant, a, a + std::min(kChunk, t1 - a)));
+    }
+  }
+  CK(cudaEventRecord(h->ev1, h->stream));
+  CK(cudaEventSynchronize(h->ev1));
+  CK(cudaGetLastError());
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (seconds) *seconds = ms * 1e-3;
+  if (iters && variant == CUPSO_ASYNC) {
+    TRY(copy_record(h, h->C.snap, h->C.live));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  for (uint32_t t = t0; t < t1; ++t) h->is_async[t] = variant == CUPSO_ASYNC;
+  h->t = t1;
+  return CUPSO_OK;
+}
+
+cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int device, uint32_t first,
+                         uint32_t count, cupso_swarm** out) {
+  if (!out) return fail(CUPSO_EINVAL, "null output handle");
+  *out = nullptr;
+  TRY(validate(p));
+  if (fid < 0 || fid >= kNumFit) {
+    std::string known;
+    for (auto n : kFitNames) known += std::string(" ") + n;
+    return fail(CUPSO_EINVAL, "unknown fitness id %d; known:%s", fid, known.c_str());
+  }
+  if (count < 1 || static_cast<uint64_t>(first) + count > p->particle_cnt)
+    return fail(CUPSO_EINVAL, "shard [%u, %u) outside the swarm of %u particles", first,
+                first + count, p->particle_cnt);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(CUPSO_ECUDA, "no CUDA device available (cuda engines have no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(CUPSO_EINVAL, "device %d out of range [0, %d)", device, ndev);
+  CK(cudaSetDevice(device));
+  auto* h = new cupso_swarm();
+  h->device = device;
+  h->fid = fid;
+  h->seed = seed;
+  h->gp = *p;
+  h->T = p->max_iter;
+  KParams& P = h->P;
+  P.w = p->inertia;
+  P.c1 = p->cognitive;
+  P.c2 = p->social;
+  P.min_pos = p->min_pos;
+  P.max_pos = p->max_pos;
+  P.min_v = p->min_v;
+  P.max_v = p->max_v;
+  P.n = count;
+  P.d = p->dims;
+  P.base = first;
+  P.gs = p->group_size;
+  P.ld = (static_cast<uint64_t>(count) + 63) / 64 * 64;
+  key_schedule(seed, P);
+  h->groups = (count + p->group_size - 1) / p->group_size;
+  h->rec_bytes = sizeof(Rec) + sizeof(double) * p->dims;
+  h->is_async.assign(h->T, 0);
+  auto bail = [&](cupso_status st) {
+    cupso_destroy(h);
+    return st;
+  };
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
+    return bail(fail(CUPSO_ECUDA, "stream/event creation failed"));
+  const size_t cells = P.ld * P.d;
+  void *pos, *vel, *pb, *pbf, *ev;
+  cupso_status st;
+  if ((st = dmalloc(h, &pos, cells * 8)) || (st = dmalloc(h, &vel, cells * 8)) ||
+      (st = dmalloc(h, &pb, cells * 8)) || (st = dmalloc(h, &pbf, P.ld * 8)) ||
+      (st = dmalloc(h, &ev, P.ld * 8)))
+    return bail(st);
+  h->S = KState{static_cast<double*>(pos), static_cast<double*>(vel), static_cast<double*>(pb),
+                static_cast<double*>(pbf)};
+  h->eval_buf = static_cast<double*>(ev);
+  // control block: snap rec, live rec, 2 shard records, counters
+  const size_t rb = (h->rec_bytes + 15) / 16 * 16;
+  const size_t ctl = 4 * rb + 64;
+  void *c, *tr, *ti, *adm, *tk, *af, *ai, *rall;
+  if ((st = dmalloc(h, &c, ctl)) || (st = dmalloc(h, &tr, h->T * 8ull)) ||
+      (st = dmalloc(h, &ti, h->T * 4ull)) || (st = dmalloc(h, &adm, h->T * 8ull)) ||
+      (st = dmalloc(h, &tk, h->T * 8ull)) || (st = dmalloc(h, &af, h->groups * 8ull + 8)) ||
+      (st = dmalloc(h, &ai, h->groups * 4ull + 4)))
+    return bail(st);
+  (void)rall;
+  h->ctl_block = static_cast<unsigned char*>(c);
+  if (cudaMemset(c, 0, ctl) != cudaSuccess) return bail(fail(CUPSO_ECUDA, "memset failed"));
+  KCtl& C = h->C;
+  C.snap = reinterpret_cast<Rec*>(h->ctl_block);
+  C.snap_pos = reinterpret_cast<double*>(h->ctl_block + sizeof(Rec));
+  C.live = reinterpret_cast<Rec*>(h->ctl_block + rb);
+  C.live_pos = reinterpret_cast<double*>(h->ctl_block + rb + sizeof(Rec));
+  h->rec_local = h->ctl_block + 2 * rb;
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(h->ctl_block + 4 * rb);
+  C.lock = ctr + 0;
+  C.ticket = ctr + 1;
+  C.bar = ctr + 2;
+  C.seq = ctr + 3;
+  C.q_count = ctr + 4;  // [3]
+  C.trace = static_cast<double*>(tr);
+  C.trace_idx = static_cast<uint32_t*>(ti);
+  C.admitted = static_cast<unsigned long long*>(adm);
+  C.trace_key = static_cast<unsigned long long*>(tk);
+  C.aux_fit = static_cast<double*>(af);
+  C.aux_idx = static_cast<uint32_t*>(ai);
+  *out = h;
+  return CUPSO_OK;
+}
+
+cupso_status init_impl(cupso_swarm* h) {
+  CK(cudaSetDevice(h->device));
+  const int blocks = static_cast<int>(std::min<uint64_t>((h->P.ld + 255) / 256, 148ull * 16));
+  cudaError_t e = cudaSuccess;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    k_init<f><<<blocks, 256, 0, h->stream>>>(h->P, h->S);
+    e = cudaGetLastError();
+  });
+  CK(e);
+  const uint32_t nb = static_cast<uint32_t>(std::min<uint64_t>((h->P.n + 255) / 256, 1024));
+  // aux arrays hold >= groups entries; use a dedicated scratch when nb exceeds them
+  double* af = h->C.aux_fit;
+  uint32_t* ai = h->C.aux_idx;
+  void *saf = nullptr, *sai = nullptr;
+  if (nb > h->groups) {
+    CK(cudaMalloc(&saf, nb * 8));
+    CK(cudaMalloc(&sai, nb * 4));
+    af = static_cast<double*>(saf);
+    ai = static_cast<uint32_t*>(sai);
+  }
+  k_argmax_blocks<<<nb, 256, 0, h->stream>>>(h->P, h->S.pbf, af, ai);
+  KCtl c2 = h->C;
+  c2.aux_fit = af;
+  c2.aux_idx = ai;
+  k_argmax_final<<<1, 1024, 0, h->stream>>>(h->P, h->S, c2, nb);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(h->C.admitted, 0, h->T * 8ull, h->stream));
+  CK(cudaMemsetAsync(h->C.trace_key, 0, h->T * 8ull, h->stream));
+  CK(cudaMemsetAsync(h->C.trace, 0, h->T * 8ull, h->stream));
+  CK(cudaMemsetAsync(h->C.trace_idx, 0xff, h->T * 4ull, h->stream));
+  Rec r;
+  CK(cudaMemcpyAsync(&r, h->C.snap, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (saf) cudaFree(saf);
+  if (sai) cudaFree(sai);
+  h->initial_fit = r.fit;
+  h->initial_particle = r.particle;
+  h->t = 0;
+  std::fill(h->is_async.begin(), h->is_async.end(), 0);
+  h->initialized = true;
+  return CUPSO_OK;
+}
+
+cupso_status download_impl(cupso_swarm* h, double* positions, double* velocities, double* fitness,
+                           double* pbest_pos, double* pbest_fit) {
+  CK(cudaSetDevice(h->device));
+  const size_t n = h->P.n, d = h->P.d, ld = h->P.ld;
+  auto rows = [&](double* dst, const double* src, size_t nrows) -> cupso_status {
+    if (!dst) return CUPSO_OK;
+    CK(cudaMemcpy2DAsync(dst, n * 8, src, ld * 8, n * 8, nrows, cudaMemcpyDeviceToHost, h->stream));
+    return CUPSO_OK;
+  };
+  TRY(rows(positions, h->S.pos, d));
+  TRY(rows(velocities, h->S.vel, d));
+  TRY(rows(pbest_pos, h->S.pb, d));
+  TRY(rows(pbest_fit, h->S.pbf, 1));
+  if (fitness) {
+    cudaError_t e = cudaSuccess;
+    dispatch_fit(h->fid, [&](auto F) {
+      constexpr int f = decltype(F)::value;
+      const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16));
+      k_eval<f><<<blocks, 256, 0, h->stream>>>(h->P, h->S.pos, h->eval_buf);
+      e = cudaGetLastError();
+    });
+    CK(e);
+    CK(cudaMemcpyAsync(fitness, h->eval_buf, n * 8, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  return CUPSO_OK;
+}
+
+cupso_status gbest_impl(cupso_swarm* h, double* fit, uint32_t* particle, double* pos) {
+  CK(cudaSetDevice(h->device));
+  std::vector<unsigned char> buf(h->rec_bytes);
+  CK(cudaMemcpyAsync(buf.data(), h->C.snap, h->rec_bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const Rec* r = reinterpret_cast<const Rec*>(buf.data());
+  if (fit) *fit = r->fit;
+  if (particle) *particle = r->particle;
+  if (pos) std::memcpy(pos, buf.data() + sizeof(Rec), sizeof(double) * h->P.d);
+  return CUPSO_OK;
+}
+
+uint64_t decode_key(unsigned long long k) {
+  return (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+}
+
+cupso_status trace_impl(cupso_swarm* h, uint32_t first, uint32_t count, double* trace,
+                        uint32_t* trace_particle, double* occupancy) {
+  if (static_cast<uint64_t>(first) + count > h->t)
+    return fail(CUPSO_EINVAL, "trace range [%u, %u) beyond completed iterations (%u)", first,
+                first + count, h->t);
+  if (!count) return CUPSO_OK;
+  CK(cudaSetDevice(h->device));
+  // the async cummax needs the prefix; fetch [0, first+count)
+  const uint32_t end = first + count;
+  std::vector<double> tr(end);
+  std::vector<uint32_t> ti(end);
+  std::vector<unsigned long long> adm(end), tk(end);
+  CK(cudaMemcpyAsync(tr.data(), h->C.trace, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(ti.data(), h->C.trace_idx, end * 4ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(adm.data(), h->C.admitted, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(tk.data(), h->C.trace_key, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  double prev = h->initial_fit;
+  for (uint32_t t = 0; t < end; ++t) {
+    if (h->is_async[t]) {
+      double v = -INFINITY;
+      if (tk[t]) {
+        const uint64_t b = decode_key(tk[t]);
+        std::memcpy(&v, &b, 8);
+      }
+      tr[t] = std::max(v, prev);  // gbest is monotone; blocks report the record they saw
+      ti[t] = kNoParticle;
+    }
+    prev = tr[t];
+  }
+  const double nrm = static_cast<double>(h->gp.particle_cnt);
+  for (uint32_t k = 0; k < count; ++k) {
+    if (trace) trace[k] = tr[first + k];
+    if (trace_particle) trace_particle[k] = ti[first + k];
+    if (occupancy) occupancy[k] = static_cast<double>(adm[first + k]) / nrm;
+  }
+  return CUPSO_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+int cupso_abi_version(void) { return CUPSO_ABI_VERSION; }
+const char* cupso_last_error(void) { return g_err.c_str(); }
+
+int cupso_fitness_id(const char* name) {
+  if (name)
+    for (int i = 0; i < kNumFit; ++i)
+      if (std::strcmp(name, kFitNames[i]) == 0) return i;
+  std::string known;
+  for (auto n : kFitNames) known += std::string(" ") + n;
+  fail(CUPSO_EINVAL, "unknown fitness '%s'; known:%s", name ? name : "(null)", known.c_str());
+  return -1;
+}
+
+const char* cupso_fitness_name(int id) { return (id >= 0 && id < kNumFit) ? kFitNames[id] : nullptr; }
+
+cupso_status cupso_fitness_box(int id, double* lo, double* hi) {
+  if (id < 0 || id >= kNumFit) return fail(CUPSO_EINVAL, "unknown fitness id %d", id);
+  if (lo) *lo = kFitLo[id];
+  if (hi) *hi = kFitHi[id];
+  return CUPSO_OK;
+}
+
+int cupso_variant_id(const char* name) {
+  if (name)
+    for (int i = 0; i < kNumVar; ++i)
+      if (std::strcmp(name, kVarNames[i]) == 0 || std::strcmp(name, kVarNames[i] + 5) == 0) return i;
+  std::string known;
+  for (auto n : kVarNames) known += std::string(" ") + n;
+  fail(CUPSO_EINVAL, "unknown engine '%s'; known:%s", name ? name : "(null)", known.c_str());
+  return -1;
+}
+
+const char* cupso_variant_name(int v) { return (v >= 0 && v < kNumVar) ? kVarNames[v] : nullptr; }
+int cupso_variant_count(void) { return kNumVar; }
+int cupso_variant_deterministic(int v) { return v >= 0 && v < CUPSO_ASYNC; }
+
+cupso_status cupso_validate_params(const cupso_params* p) { return validate(p); }
+
+cupso_status cupso_make_params(int fid, uint32_t particle_cnt, uint32_t dims, uint32_t max_iter,
+                               uint32_t group_size, cupso_params* out) {
+  if (fid < 0 || fid >= kNumFit) return fail(CUPSO_EINVAL, "unknown fitness id %d", fid);
+  if (!out) return fail(CUPSO_EINVAL, "null output");
+  cupso_params p{};  // params.hpp:52-66
+  p.inertia = 1.0;
+  p.cognitive = 2.0;
+  p.social = 2.0;
+  p.min_pos = kFitLo[fid];
+  p.max_pos = kFitHi[fid];
+  p.max_v = (kFitHi[fid] - kFitLo[fid]) / 2.0;
+  p.min_v = -p.max_v;
+  p.particle_cnt = particle_cnt;
+  p.dims = dims;
+  p.max_iter = max_iter;
+  p.group_size = group_size;
+  *out = p;
+  return validate(&p);
+}
+
+int cupso_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+cupso_status cupso_create(const cupso_params* p, int fid, uint64_t seed, int device, cupso_swarm** out) {
+  if (!p) return fail(CUPSO_EINVAL, "pso_params: null");
+  return create_impl(p, fid, seed, device, 0, p->particle_cnt, out);
+}
+
+cupso_status cupso_create_shard(const cupso_params* p, int fid, uint64_t seed, int device,
+                                uint32_t first, uint32_t count, cupso_swarm** out) {
+  if (!p) return fail(CUPSO_EINVAL, "pso_params: null");
+  return create_impl(p, fid, seed, device, first, count, out);
+}
+
+cupso_status cupso_destroy(cupso_swarm* h) {
+  if (!h) return CUPSO_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return CUPSO_OK;
+}
+
+cupso_status cupso_init(cupso_swarm* h) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  return init_impl(h);
+}
+
+cupso_status cupso_step(cupso_swarm* h, int variant, uint32_t iters, double* device_seconds) {
+  return do_step(h, variant, iters, device_seconds);
+}
+
+cupso_status cupso_synchronize(cupso_swarm* h) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->stream));
+  return CUPSO_OK;
+}
+
+uint32_t cupso_iteration(const cupso_swarm* h) { return h ? h->t : 0; }
+
+cupso_status cupso_get_gbest(cupso_swarm* h, double* fit, uint32_t* particle, double* pos) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  return gbest_impl(h, fit, particle, pos);
+}
+
+cupso_status cupso_get_initial_gbest(cupso_swarm* h, double* fit, uint32_t* particle) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  if (fit) *fit = h->initial_fit;
+  if (particle) *particle = h->initial_particle;
+  return CUPSO_OK;
+}
+
+cupso_status cupso_get_trace(cupso_swarm* h, uint32_t first, uint32_t count, double* trace,
+                             uint32_t* trace_particle, double* occupancy) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  return trace_impl(h, first, count, trace, trace_particle, occupancy);
+}
+
+cupso_status cupso_download_state(cupso_swarm* h, double* positions, double* velocities,
+                                  double* fitness, double* pbest_pos, double* pbest_fit) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  return download_impl(h, positions, velocities, fitness, pbest_pos, pbest_fit);
+}
+
+cupso_status cupso_upload_state(cupso_swarm* h, uint32_t iteration, const double* positions,
+                                const double* velocities, const double* pbest_pos,
+                                const double* pbest_fit, double gbest_fit, uint32_t gbest_particle,
+                                const double* gbest_pos) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  if (!positions || !velocities || !pbest_pos || !pbest_fit || !gbest_pos)
+    return fail(CUPSO_EINVAL, "cupso_upload_state: all state arrays are required");
+  if (iteration > h->T) return fail(CUPSO_EINVAL, "iteration %u beyond max_iter %u", iteration, h->T);
+  CK(cudaSetDevice(h->device));
+  const size_t n = h->P.n, d = h->P.d, ld = h->P.ld;
+  // neutral padding, then the rows
+  if (!h->initialized) TRY(init_impl(h));
+  auto rows = [&](double* dst, const double* src, size_t nrows) -> cupso_status {
+    CK(cudaMemcpy2DAsync(dst, ld * 8, src, n * 8, n * 8, nrows, cudaMemcpyHostToDevice, h->stream));
+    return CUPSO_OK;
+  };
+  TRY(rows(h->S.pos, positions, d));
+  TRY(rows(h->S.vel, velocities, d));
+  TRY(rows(h->S.pb, pbest_pos, d));
+  TRY(rows(h->S.pbf, pbest_fit, 1));
+  std::vector<unsigned char> rec(h->rec_bytes);
+  Rec r{gbest_fit, gbest_particle, 0u};
+  std::memcpy(rec.data(), &r, sizeof r);
+  std::memcpy(rec.data() + sizeof(Rec), gbest_pos, d * 8);
+  CK(cudaMemcpyAsync(h->C.snap, rec.data(), h->rec_bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->C.live, rec.data(), h->rec_bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->t = iteration;
+  h->initialized = true;
+  return CUPSO_OK;
+}
+
+cupso_status cupso_device_state(cupso_swarm* h, double** pos, double** vel, double** pbest_pos,
+                                double** pbest_fit, uint64_t* ld) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  if (pos) *pos = h->S.pos;
+  if (vel) *vel = h->S.vel;
+  if (pbest_pos) *pbest_pos = h->S.pb;
+  if (pbest_fit) *pbest_fit = h->S.pbf;
+  if (ld) *ld = h->P.ld;
+  return CUPSO_OK;
+}
+
+size_t cupso_device_bytes(const cupso_swarm* h) {
+  if (!h) return 0;
+  return h->P.ld * (3ull * h->P.d + 2) * 8;
+}
+
+int cupso_sync_grid_blocks(const cupso_swarm* h) { return h ? h->sync_grid : 0; }
+
+size_t cupso_record_bytes(uint32_t dims) { return sizeof(Rec) + sizeof(double) * dims; }
+
+cupso_status cupso_shard_propose_device(cupso_swarm* h, void* record_dev) {
+  if (!h || !record_dev) return fail(CUPSO_EINVAL, "null argument");
+  if (!h->initialized) return fail(CUPSO_ELOGIC, "propose before cupso_init");
+  if (h->t >= h->T) return fail(CUPSO_EINVAL, "swarm already ran max_iter (%u) iterations", h->T);
+  CK(cudaSetDevice(h->device));
+  return propose_launch(h, h->t, static_cast<unsigned char*>(record_dev));
+}
+
+cupso_status cupso_shard_propose(cupso_swarm* h, void* record_host) {
+  if (!h || !record_host) return fail(CUPSO_EINVAL, "null argument");
+  TRY(cupso_shard_propose_device(h, h->rec_local));
+  CK(cudaMemcpyAsync(record_host, h->rec_local, h->rec_bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return CUPSO_OK;
+}
+
+cupso_status cupso_shard_commit_device(cupso_swarm* h, const void* records_dev, uint32_t nrecords) {
+  if (!h || !records_dev) return fail(CUPSO_EINVAL, "null argument");
+  if (h->t >= h->T) return fail(CUPSO_EINVAL, "swarm already ran max_iter (%u) iterations", h->T);
+  CK(cudaSetDevice(h->device));
+  TRY(commit_launch(h, h->t, static_cast<const unsigned char*>(records_dev), nrecords));
+  h->is_async[h->t] = 0;
+  h->t += 1;
+  return CUPSO_OK;
+}
+
+cupso_status cupso_shard_commit(cupso_swarm* h, const void* records_host, uint32_t nrecords) {
+  if (!h || !records_host) return fail(CUPSO_EINVAL, "null argument");
+  CK(cudaSetDevice(h->device));
+  void* d = nullptr;
+  CK(cudaMallocAsync(&d, h->rec_bytes * nrecords, h->stream));
+  CK(cudaMemcpyAsync(d, records_host, h->rec_bytes * nrecords, cudaMemcpyHostToDevice, h->stream));
+  cupso_status st = cupso_shard_commit_device(h, d, nrecords);
+  cudaFreeAsync(d, h->stream);
+  CK(cudaStreamSynchronize(h->stream));
+  return st;
+}
+
+cupso_status cupso_nccl_unique_id(void* out128) {
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(CUPSO_ERUNTIME, "libnccl.so.2 not loadable");
+  const int r = api.getUniqueId(out128);
+  if (r != 0) return fail(CUPSO_ERUNTIME, "ncclGetUniqueId failed (%d)", r);
+  return CUPSO_OK;
+}
+
+cupso_status cupso_nccl_init(cupso_swarm* h, const void* unique_id, int nranks, int rank) {
+  if (!h || !unique_id) return fail(CUPSO_EINVAL, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CUPSO_EINVAL, "bad rank %d of %d", rank, nranks);
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(CUPSO_ERUNTIME, "libnccl.so.2 not loadable");
+  CK(cudaSetDevice(h->device));
+  NcclUid uid;
+  std::memcpy(uid.internal, unique_id, 128);
+  void* comm = nullptr;
+  const int r = reinterpret_cast<CommInitRankFn>(api.commInitRank)(&comm, nranks, uid, rank);
+  if (r != 0)
+    return fail(CUPSO_ERUNTIME, "ncclCommInitRank failed: %s", api.getErrorString ? api.getErrorString(r) : "?");
+  void* all = nullptr;
+  TRY(dmalloc(h, &all, h->rec_bytes * nranks));
+  h->rec_all = static_cast<unsigned char*>(all);
+  h->comm = comm;
+  h->nranks = nranks;
+  h->rank = rank;
+  return CUPSO_OK;
+}
+
+void* cupso_stream(cupso_swarm* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+// ------------------------------------------------------------- one-shot run
+cupso_status cupso_run(const cupso_params* p, int fid, uint64_t seed, int variant, int device,
+                       cupso_observer_fn observer, void* user, cupso_result* out) {
+  if (!out) return fail(CUPSO_EINVAL, "null result");
+  TRY(validate(p));
+  if (variant < 0 || variant >= kNumVar) return fail(CUPSO_EINVAL, "unknown variant %d", variant);
+  cupso_swarm* h = nullptr;
+  TRY(cupso_create(p, fid, seed, device, &h));
+  struct Guard {
+    cupso_swarm* h;
+    ~Guard() { cupso_destroy(h); }
+  } guard{h};
+  TRY(init_impl(h));
+  out->initial_gbest_fit = h->initial_fit;
+  double total = 0.0;
+  if (!observer) {
+    TRY(do_step(h, variant, p->max_iter, &total));
+  } else {
+    const size_t n = p->particle_cnt, d = p->dims;
+    std::vector<double> pos(n * d), vel(n * d), fit(n), pb(n * d), pbf(n), gpos(d);
+    for (uint32_t t = 0; t < p->max_iter; ++t) {
+      double s = 0.0;
+      TRY(do_step(h, variant, 1, &s));
+      total += s;
+      TRY(download_impl(h, pos.data(), vel.data(), fit.data(), pb.data(), pbf.data()));
+      cupso_state_view v{};
+      v.particle_cnt = p->particle_cnt;
+      v.dims = p->dims;
+      v.positions = pos.data();
+      v.velocities = vel.data();
+      v.fitness = fit.data();
+      v.pbest_pos = pb.data();
+      v.pbest_fit = pbf.data();
+      TRY(gbest_impl(h, &v.gbest_fit, &v.gbest_particle, gpos.data()));
+      v.gbest_pos = gpos.data();
+      observer(t, &v, user);
+    }
+  }
+  out->compute_seconds = total;
+  TRY(gbest_impl(h, &out->gbest_fit, &out->gbest_particle, out->gbest_pos));
+  TRY(trace_impl(h, 0, p->max_iter, out->trace, out->trace_particle,
+                 (variant == CUPSO_REDUCTION || variant == CUPSO_UNROLLED) ? nullptr
+                                                                          : out->queue_occupancy));
+  out->has_occupancy = !(variant == CUPSO_REDUCTION || variant == CUPSO_UNROLLED);
+  return CUPSO_OK;
+}
+
+// ------------------------------------------------------ self-test hooks
+}  // extern "C"
+
+namespace {
+__global__ void k_philox_batch(const uint32_t* ctr4, const uint32_t* key2, uint32_t* out4, size_t n) {
+  for (size_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    KParams P{};
+    uint32_t k0 = key2[2 * k], k1 = key2[2 * k + 1];
+    for (int r = 0; r < 10; ++r) {
+      P.k0[r] = k0;
+      P.k1[r] = k1;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t c0 = ctr4[4 * k], c1 = ctr4[4 * k + 1], c2 = ctr4[4 * k + 2], c3 = ctr4[4 * k + 3];
+    philox10(c0, c1, c2, c3, P);
+    out4[4 * k] = c0;
+    out4[4 * k + 1] = c1;
+    out4[4 * k + 2] = c2;
+    out4[4 * k + 3] = c3;
+  }
+}
+__global__ void k_uniform_batch(KParams P, const uint32_t* draw4, double* out, size_t n) {
+  for (size_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    out[k] = uniform01(P, draw4[4 * k], draw4[4 * k + 1], draw4[4 * k + 2], draw4[4 * k + 3]);
+}
+__global__ void k_kin_batch(KParams P, const double* v, const double* x, const double* pb,
+                            const double* g, const double* r1, const double* r2, double* vo,
+                            double* xo, size_t n) {
+  for (size_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const double nv = vel_step(P, v[k], x[k], pb[k], g[k], r1[k], r2[k]);
+    vo[k] = nv;
+    xo[k] = pos_step(P, x[k], nv);
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n * sizeof(T) + 16); }
+};
+}  // namespace
+
+extern "C" {
+
+cupso_status cupso_philox_batch(int device, const uint32_t* ctr4, const uint32_t* key2, uint32_t* out4,
+                                size_t n) {
+  if (!n) return CUPSO_OK;
+  CK(cudaSetDevice(device));
+  DevBuf<uint32_t> c, k, o;
+  CK(c.alloc(4 * n));
+  CK(k.alloc(2 * n));
+  CK(o.alloc(4 * n));
+  CK(cudaMemcpy(c.p, ctr4, 16 * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(k.p, key2, 8 * n, cudaMemcpyHostToDevice));
+  k_philox_batch<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256>>>(c.p, k.p, o.p, n);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out4, o.p, 16 * n, cudaMemcpyDeviceToHost));
+  return CUPSO_OK;
+}
+
+cupso_status cupso_uniform01_batch(int device, uint64_t seed, const uint32_t* draw4, double* out, size_t n) {
+  if (!n) return CUPSO_OK;
+  CK(cudaSetDevice(device));
+  KParams P{};
+  key_schedule(seed, P);
+  DevBuf<uint32_t> dr;
+  DevBuf<double> o;
+  CK(dr.alloc(4 * n));
+  CK(o.alloc(n));
+  CK(cudaMemcpy(dr.p, draw4, 16 * n, cudaMemcpyHostToDevice));
+  k_uniform_batch<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256>>>(P, dr.p, o.p, n);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, o.p, 8 * n, cudaMemcpyDeviceToHost));
+  return CUPSO_OK;
+}
+
+cupso_status cupso_eval_fitness(int device, int fid, const double* x, uint32_t n, uint32_t dims,
+                                double* out) {
+  if (fid < 0 || fid >= kNumFit) return fail(CUPSO_EINVAL, "unknown fitness id %d", fid);
+  if (!n) return CUPSO_OK;
+  CK(cudaSetDevice(device));
+  KParams P{};
+  P.n = n;
+  P.d = dims;
+  P.ld = n;
+  DevBuf<double> dx, o;
+  CK(dx.alloc(static_cast<size_t>(n) * dims));
+  CK(o.alloc(n));
+  CK(cudaMemcpy(dx.p, x, 8ull * n * dims, cudaMemcpyHostToDevice));
+  cudaError_t e = cudaSuccess;
+  dispatch_fit(fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    k_eval<f><<<(n + 255) / 256, 256>>>(P, dx.p, o.p);
+    e = cudaGetLastError();
+  });
+  CK(e);
+  CK(cudaMemcpy(out, o.p, 8ull * n, cudaMemcpyDeviceToHost));
+  return CUPSO_OK;
+}
+
+cupso_status cupso_eval_kinematics(int device, const cupso_params* p, const double* v, const double* x,
+                                   const double* pbest_x, const double* gbest_x, const double* r1,
+                                   const double* r2, double* v_out, double* x_out, size_t n) {
+  if (!p) return fail(CUPSO_EINVAL, "pso_params: null");
+  if (!n) return CUPSO_OK;
+  CK(cudaSetDevice(device));
+  KParams P{};
+  P.w = p->inertia;
+  P.c1 = p->cognitive;
+  P.c2 = p->social;
+  P.min_pos = p->min_pos;
+  P.max_pos = p->max_pos;
+  P.min_v = p->min_v;
+  P.max_v = p->max_v;
+  DevBuf<double> b;
+  CK(b.alloc(8 * n));
+  const double* srcs[6] = {v, x, pbest_x, gbest_x, r1, r2};
+  for (int i = 0; i < 6; ++i) CK(cudaMemcpy(b.p + i * n, srcs[i], 8 * n, cudaMemcpyHostToDevice));
+  k_kin_batch<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256>>>(
+      P, b.p, b.p + n, b.p + 2 * n, b.p + 3 * n, b.p + 4 * n, b.p + 5 * n, b.p + 6 * n, b.p + 7 * n, n);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(v_out, b.p + 6 * n, 8 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(x_out, b.p + 7 * n, 8 * n, cudaMemcpyDeviceToHost));
+  return CUPSO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+// cupso_device.cuh -- device-side building blocks of the PSO step (sm_100a).
+//
+// Every function here restates one reference function bit for bit:
+//   philox10 / uniform01  <- rng.hpp:36-62
+//   clampd / vel_step / pos_step <- swarm.hpp:56-77
+//   Fit* accumulators     <- fitness.hpp:47-85 (+ harness Rastrigin)
+//   beats                 <- engine.hpp:38-41
+// FP64 arithmetic uses explicit _rn intrinsics in the reference's evaluation
+// order, and the whole library is compiled with -fmad=false: the reference
+// builds with -ffp-contract=off (proj/CMakeLists.txt:17-20), so an FMA
+// contraction here would change the trajectory's last bits.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cupso {
+
+constexpr uint32_t kNoParticle = 0xffffffffu;  // swarm.hpp:16
+
+// Kernel-uniform run parameters, passed by value (lives in the constant bank).
+struct KParams {
+  double w, c1, c2;                 // inertia, cognitive, social
+  double min_pos, max_pos, min_v, max_v;
+  uint64_t ld;                      // padded leading dimension (particles per axis row)
+  uint32_t n;                       // particles in this swarm / shard
+  uint32_t d;                       // dims
+  uint32_t base;                    // global index of local particle 0 (multi-GPU shards)
+  uint32_t gs;                      // group_size for the classic engines
+  uint32_t k0[10], k1[10];          // Philox key schedule (seed-only, precomputed on host)
+};
+
+// Axis-major SoA state, row stride ld (flat index = axis*ld + i).
+struct KState {
+  double* pos;
+  double* vel;
+  double* pb;    // pbest positions
+  double* pbf;   // pbest fitness
+};
+
+// ---------------------------------------------------------------- RNG
+__device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                         const KParams& P) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ P.k0[r];
+    const uint32_t n2 = hi0 ^ c3 ^ P.k1[r];
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+}
+
+// uniform01(key, {t, i, axis, slot}) = ((w0<<32 | w1) >> 11) * 2^-53, exact.
+__device__ __forceinline__ double uniform01(const KParams& P, uint32_t t, uint32_t i, uint32_t axis,
+                                            uint32_t slot) {
+  uint32_t c0 = t, c1 = i, c2 = axis, c3 = slot;
+  philox10(c0, c1, c2, c3, P);
+  const uint64_t bits53 = (static_cast<uint64_t>(c0) << 21) | (c1 >> 11);
+  return __dmul_rn(__ull2double_rn(bits53), 0x1.0p-53);
+}
+
+// ---------------------------------------------------------- kinematics
+// std::clamp(v, lo, hi): v < lo ? lo : (hi < v ? hi : v)  -- keeps -0.0 and NaN as the CPU does
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return v < lo ? lo : (hi < v ? hi : v);
+}
+
+// ((w*v) + ((c1*r1)*(pb-x))) + ((c2*r2)*(g-x)), saturated (swarm.hpp:67-72)
+__device__ __forceinline__ double vel_step(const KParams& P, double v, double x, double pb, double g,
+                                           double r1, double r2) {
+  const double a = __dmul_rn(P.w, v);
+  const double b = __dmul_rn(__dmul_rn(P.c1, r1), __dsub_rn(pb, x));
+  const double c = __dmul_rn(__dmul_rn(P.c2, r2), __dsub_rn(g, x));
+  return clampd(__dadd_rn(__dadd_rn(a, b), c), P.min_v, P.max_v);
+}
+
+__device__ __forceinline__ double pos_step(const KParams& P, double x, double v) {
+  return clampd(__dadd_rn(x, v), P.min_pos, P.max_pos);
+}
+
+// ------------------------------------------------------------- fitness
+// Accumulators fed one axis at a time in ascending order (fitness.hpp:26-27).
+enum FitId : int { kCubic = 0, kSphere = 1, kRosenbrock = 2, kGriewank = 3, kRastrigin = 4 };
+
+template <int F>
+struct Fit;
+
+template <>
+struct Fit<kCubic> {  // fitness.hpp:47-54
+  double acc = 0.0;
+  __device__ __forceinline__ void add(double v, uint32_t) {
+    const double t = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(__dsub_rn(v, 0.8), v), 1000.0), v), 8000.0);
+    acc = __dadd_rn(acc, t);
+  }
+  __device__ __forceinline__ double value() const { return acc; }
+};
+
+template <>
+struct Fit<kSphere> {  // fitness.hpp:57-61
+  double acc = 0.0;
+  __device__ __forceinline__ void add(double v, uint32_t) { acc = __dadd_rn(acc, __dmul_rn(v, v)); }
+  __device__ __forceinline__ double value() const { return -acc; }
+};
+
+template <>
+struct Fit<kRosenbrock> {  // fitness.hpp:65-73: pairs (x_d, x_{d+1}) in ascending d
+  double acc = 0.0;
+  double prev = 0.0;
+  __device__ __forceinline__ void add(double v, uint32_t axis) {
+    if (axis > 0) {
+      const double a = __dsub_rn(v, __dmul_rn(prev, prev));
+      const double b = __dsub_rn(1.0, prev);
+      acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(__dmul_rn(100.0, a), a), __dmul_rn(b, b)));
+    }
+    prev = v;
+  }
+  __device__ __forceinline__ double value() const { return -acc; }
+};
+
+template <>
+struct Fit<kGriewank> {  // fitness.hpp:77-85 (cos: CUDA's, <=1-2 ulp from glibc)
+  double sum = 0.0;
+  double prod = 1.0;
+  __device__ __forceinline__ void add(double v, uint32_t axis) {
+    sum = __dadd_rn(sum, __ddiv_rn(__dmul_rn(v, v), 4000.0));
+    prod = __dmul_rn(prod, cos(__ddiv_rn(v, __dsqrt_rn(static_cast<double>(axis + 1)))));
+  }
+  __device__ __forceinline__ double value() const { return -__dsub_rn(__dadd_rn(1.0, sum), prod); }
+};
+
+template <>
+struct Fit<kRastrigin> {  // harness fitness_fn (oracle/pso_oracle.c:rastrigin)
+  double acc = 0.0;
+  __device__ __forceinline__ void add(double v, uint32_t) {
+    const double t = __dadd_rn(__dsub_rn(__dmul_rn(v, v), __dmul_rn(10.0, cos(__dmul_rn(6.283185307179586, v)))), 10.0);
+    acc = __dadd_rn(acc, t);
+  }
+  __device__ __forceinline__ double value() const { return -acc; }
+};
+
+// ------------------------------------------------------ (fit, idx) order
+// engine.hpp:38-41: fitness descending, ties to the lower particle index.
+__device__ __forceinline__ bool beats(double f, uint32_t i, double F, uint32_t I) {
+  return f > F || (f == F && i < I);
+}
+
+// Butterfly argmax over a full warp; every lane ends with the winner.
+__device__ __forceinline__ void warp_argmax(double& f, uint32_t& i) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double of = __shfl_xor_sync(0xffffffffu, f, off);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, i, off);
+    if (beats(of, oi, f, i)) {
+      f = of;
+      i = oi;
+    }
+  }
+}
+
+__device__ __forceinline__ void warp_argmax3(double& f, uint32_t& i, uint32_t& s) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double of = __shfl_xor_sync(0xffffffffu, f, off);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, i, off);
+    const uint32_t os = __shfl_xor_sync(0xffffffffu, s, off);
+    if (beats(of, oi, f, i)) {
+      f = of;
+      i = oi;
+      s = os;
+    }
+  }
+}
+
+// --------------------------------------------------- one particle's step
+// advance_particle (swarm.hpp:115-131) for one particle, scalar accesses.
+// Returns the new fitness; updates pbest in place on strict improvement.
+template <int F>
+__device__ __forceinline__ double advance_one(const KParams& P, const KState& S, uint32_t t,
+                                              uint32_t li, const double* __restrict__ gpos) {
+  const uint32_t gi = P.base + li;
+  Fit<F> fit;
+  for (uint32_t a = 0; a < P.d; ++a) {
+    const size_t at = static_cast<size_t>(a) * P.ld + li;
+    const double r1 = uniform01(P, t, gi, a, 0);
+    const double r2 = uniform01(P, t, gi, a, 1);
+    const double x = S.pos[at];
+    const double v = vel_step(P, S.vel[at], x, S.pb[at], gpos[a], r1, r2);
+    const double nx = pos_step(P, x, v);
+    S.vel[at] = v;
+    S.pos[at] = nx;
+    fit.add(nx, a);
+  }
+  const double f = fit.value();
+  if (f > S.pbf[li]) {  // update_pbest, strict > (swarm.hpp:100-108)
+    S.pbf[li] = f;
+    for (uint32_t a = 0; a < P.d; ++a) {
+      const size_t at = static_cast<size_t>(a) * P.ld + li;
+      S.pb[at] = S.pos[at];
+    }
+  }
+  return f;
+}
+
+// Two adjacent particles (li, li+1) per thread with 128-bit accesses: one
+// LDG.128 per array per axis covers both, and the two Philox streams give
+// the scheduler independent work. li must be even (ld is a multiple of 64).
+template <int F>
+__device__ __forceinline__ void advance_pair(const KParams& P, const KState& S, uint32_t t,
+                                             uint32_t li, const double* __restrict__ gpos,
+                                             double& fa, double& fb) {
+  const uint32_t ga = P.base + li;
+  const uint32_t gb = ga + 1;
+  Fit<F> A, B;
+  for (uint32_t a = 0; a < P.d; ++a) {
+    const size_t at = static_cast<size_t>(a) * P.ld + li;
+    const double2 x = *reinterpret_cast<const double2*>(S.pos + at);
+    const double2 v = *reinterpret_cast<const double2*>(S.vel + at);
+    const double2 pb = *reinterpret_cast<const double2*>(S.pb + at);
+    const double g = gpos[a];
+    const double r1a = uniform01(P, t, ga, a, 0);
+    const double r2a = uniform01(P, t, ga, a, 1);
+    const double r1b = uniform01(P, t, gb, a, 0);
+    const double r2b = uniform01(P, t, gb, a, 1);
+    double2 nv, nx;
+    nv.x = vel_step(P, v.x, x.x, pb.x, g, r1a, r2a);
+    nv.y = vel_step(P, v.y, x.y, pb.y, g, r1b, r2b);
+    nx.x = pos_step(P, x.x, nv.x);
+    nx.y = pos_step(P, x.y, nv.y);
+    *reinterpret_cast<double2*>(S.vel + at) = nv;
+    *reinterpret_cast<double2*>(S.pos + at) = nx;
+    A.add(nx.x, a);
+    B.add(nx.y, a);
+  }
+  fa = A.value();
+  fb = B.value();
+  const double2 pbf = *reinterpret_cast<const double2*>(S.pbf + li);
+  const bool ua = fa > pbf.x && li < P.n;
+  const bool ub = fb > pbf.y && li + 1 < P.n;
+  if (ua | ub) {  // rare after warm-up: re-read the just-written positions
+    if (ua) S.pbf[li] = fa;
+    if (ub) S.pbf[li + 1] = fb;
+    for (uint32_t a = 0; a < P.d; ++a) {
+      const size_t at = static_cast<size_t>(a) * P.ld + li;
+      if (ua) S.pb[at] = S.pos[at];
+      if (ub) S.pb[at + 1] = S.pos[at + 1];
+    }
+  }
+}
+
+// Fitness of particle li's current position (for state export / init).
+template <int F>
+__device__ __forceinline__ double eval_position(const KParams& P, const double* __restrict__ pos,
+                                                uint32_t li) {
+  Fit<F> fit;
+  for (uint32_t a = 0; a < P.d; ++a) fit.add(pos[static_cast<size_t>(a) * P.ld + li], a);
+  return fit.value();
+}
+
+}  // namespace cupso

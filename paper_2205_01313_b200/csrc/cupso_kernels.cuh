@@ -1,0 +1,873 @@
+// cupso_kernels.cuh -- the PSO-step kernels for sm_100a.
+//
+// Classic per-iteration kernels (the paper's four GPU algorithms, one
+// particle per thread, block = group_size, launched twice / once per
+// iteration inside a CUDA graph):
+//   k_classic_step<F, kTree|kTreeUnrolled>  + k_classic_fold   (reduction baseline)
+//   k_classic_step<F, kQueue>               + k_classic_fold   (queue)
+//   k_classic_step<F, kQueueLock>                              (queue-lock, fused)
+// B200-native persistent kernels (two particles per thread, 128-bit accesses):
+//   k_sync<F>   one cooperative launch for the whole run; per iteration a
+//               warp-ballot filter, warp-shuffle argmax, block queue in smem,
+//               a grid-level candidate queue and one grid barrier. Every block
+//               resolves the (tiny) grid queue itself, so no second barrier.
+//   k_async<F>  free-running blocks; the global best is a seqlock record
+//               whose writers take it with a CAS on the version word.
+//   k_propose<F> + k_commit: one iteration of a shard (multi-GPU exchange).
+#pragma once
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "cupso_device.cuh"
+
+namespace cupso {
+
+constexpr int kTree = 0, kTreeUnrolled = 1, kQueue = 2, kQueueLock = 3;
+constexpr int kSyncThreads = 256;
+constexpr int kSyncWarps = kSyncThreads / 32;
+
+struct Rec {  // global-best record header; followed by pos[d] where stored as a record
+  double fit;
+  uint32_t particle;
+  uint32_t admitted;
+};
+
+struct KCtl {
+  Rec* snap;                      // iteration-start snapshot (read-only inside a step)
+  double* snap_pos;               // [d]
+  Rec* live;                      // queue-lock / async live record
+  double* live_pos;               // [d]
+  double* trace;                  // [T]
+  uint32_t* trace_idx;            // [T]
+  unsigned long long* admitted;   // [T] particles passing the snapshot filter
+  unsigned long long* trace_key;  // [T] async: order-preserving max of the observed gbest
+  double* aux_fit;                // [groups]
+  uint32_t* aux_idx;              // [groups]
+  uint32_t* lock;                 // queue-lock spin lock word
+  uint32_t* ticket;               // last-block-done counter
+  uint32_t* bar;                  // grid barrier counter
+  uint32_t* seq;                  // async seqlock version
+  uint32_t* q_count;              // [3] grid queue fill counters
+  double* q_fit;                  // [3*cap]
+  uint32_t* q_idx;                // [3*cap]
+  double* q_pos;                  // [3*cap*d]
+  uint32_t q_cap;
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// A spin that never returns means a co-residency bug; trap instead of hanging the GPU.
+constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Order-preserving map double -> u64 (for the async trace max).
+__device__ __forceinline__ unsigned long long order_key(double f) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(f));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// ------------------------------------------------------------------ init
+// init_swarm (swarm.hpp:136-171): uniform_range draws in slots 2/3 at
+// iteration 0, pbest = position, fitness evaluated. Padding lanes get a
+// neutral state (zeros, pbest_fit = -inf).
+template <int F>
+__global__ void k_init(KParams P, KState S) {
+  const double ninf = -INFINITY;
+  for (uint64_t li = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; li < P.ld;
+       li += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (li < P.n) {
+      const uint32_t gi = P.base + static_cast<uint32_t>(li);
+      Fit<F> fit;
+      for (uint32_t a = 0; a < P.d; ++a) {
+        const size_t at = static_cast<size_t>(a) * P.ld + li;
+        const double ux = uniform01(P, 0, gi, a, 2);
+        const double uv = uniform01(P, 0, gi, a, 3);
+        const double x = __dadd_rn(P.min_pos, __dmul_rn(ux, __dsub_rn(P.max_pos, P.min_pos)));
+        const double v = __dadd_rn(P.min_v, __dmul_rn(uv, __dsub_rn(P.max_v, P.min_v)));
+        S.pos[at] = x;
+        S.vel[at] = v;
+        S.pb[at] = x;
+        fit.add(x, a);
+      }
+      S.pbf[li] = fit.value();
+    } else {
+      for (uint32_t a = 0; a < P.d; ++a) {
+        const size_t at = static_cast<size_t>(a) * P.ld + li;
+        S.pos[at] = 0.0;
+        S.vel[at] = 0.0;
+        S.pb[at] = 0.0;
+      }
+      S.pbf[li] = ninf;
+    }
+  }
+}
+
+// Block argmax over pbest_fit (first strict max == beats order) -> aux.
+__global__ void k_argmax_blocks(KParams P, const double* __restrict__ vals, double* aux_fit,
+                                uint32_t* aux_idx) {
+  __shared__ double sf[32];
+  __shared__ uint32_t si[32];
+  double f = -INFINITY;
+  uint32_t i = kNoParticle;
+  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < P.n; li += gridDim.x * blockDim.x) {
+    const double v = vals[li];
+    if (beats(v, P.base + li, f, i)) {
+      f = v;
+      i = P.base + li;
+    }
+  }
+  warp_argmax(f, i);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sf[warp] = f;
+    si[warp] = i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nw = blockDim.x >> 5;
+    f = lane < nw ? sf[lane] : -INFINITY;
+    i = lane < nw ? si[lane] : kNoParticle;
+    warp_argmax(f, i);
+    if (lane == 0) {
+      aux_fit[blockIdx.x] = f;
+      aux_idx[blockIdx.x] = i;
+    }
+  }
+}
+
+// Fold aux -> initial gbest record (snapshot and live), gather position.
+__global__ void k_argmax_final(KParams P, KState S, KCtl C, uint32_t nblocks) {
+  __shared__ double sf[32];
+  __shared__ uint32_t si[32];
+  double f = -INFINITY;
+  uint32_t i = kNoParticle;
+  for (uint32_t k = threadIdx.x; k < nblocks; k += blockDim.x) {
+    if (beats(C.aux_fit[k], C.aux_idx[k], f, i)) {
+      f = C.aux_fit[k];
+      i = C.aux_idx[k];
+    }
+  }
+  warp_argmax(f, i);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sf[warp] = f;
+    si[warp] = i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nw = blockDim.x >> 5;
+    f = lane < nw ? sf[lane] : -INFINITY;
+    i = lane < nw ? si[lane] : kNoParticle;
+    warp_argmax(f, i);
+    if (lane == 0) {
+      sf[0] = f;
+      si[0] = i;
+    }
+  }
+  __syncthreads();
+  f = sf[0];
+  i = si[0];
+  const bool adopt = f > -INFINITY;  // swarm.hpp:165 strict > against the -inf sentinel
+  for (uint32_t a = threadIdx.x; a < P.d; a += blockDim.x) {
+    const double x = adopt ? S.pb[static_cast<size_t>(a) * P.ld + (i - P.base)] : 0.0;
+    C.snap_pos[a] = x;
+    C.live_pos[a] = x;
+  }
+  if (threadIdx.x == 0) {
+    const Rec r{adopt ? f : -INFINITY, adopt ? i : kNoParticle, 0u};
+    *C.snap = r;
+    *C.live = r;
+  }
+}
+
+template <int F>
+__global__ void k_eval(KParams P, const double* __restrict__ pos, double* out) {
+  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < P.n; li += gridDim.x * blockDim.x)
+    out[li] = eval_position<F>(P, pos, li);
+}
+
+// ------------------------------------------------- classic tree helpers
+// reduce_round (engine.hpp:45-55) over the padded smem arrays, looped tree.
+__device__ __forceinline__ void tree_looped(double* wf, uint32_t* wi, uint32_t lane, uint32_t padded) {
+  for (uint32_t stride = padded >> 1; stride >= 1; stride >>= 1) {
+    if (lane < stride && beats(wf[lane + stride], wi[lane + stride], wf[lane], wi[lane])) {
+      wf[lane] = wf[lane + stride];
+      wi[lane] = wi[lane + stride];
+    }
+    __syncthreads();
+  }
+}
+
+// Straight-line variant for padded in {32,64,128,256} (engine_reduction.hpp:48-76).
+template <uint32_t S>
+__device__ __forceinline__ void round_at(double* wf, uint32_t* wi, uint32_t lane) {
+  if (lane < S && beats(wf[lane + S], wi[lane + S], wf[lane], wi[lane])) {
+    wf[lane] = wf[lane + S];
+    wi[lane] = wi[lane + S];
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void tree_unrolled(double* wf, uint32_t* wi, uint32_t lane, uint32_t padded) {
+  switch (padded) {
+    case 256: round_at<128>(wf, wi, lane); [[fallthrough]];
+    case 128: round_at<64>(wf, wi, lane); [[fallthrough]];
+    case 64: round_at<32>(wf, wi, lane); [[fallthrough]];
+    case 32:
+      round_at<16>(wf, wi, lane);
+      round_at<8>(wf, wi, lane);
+      round_at<4>(wf, wi, lane);
+      round_at<2>(wf, wi, lane);
+      round_at<1>(wf, wi, lane);
+      break;
+    default: tree_looped(wf, wi, lane, padded);
+  }
+}
+
+// Global spin lock (Alg. 3 atomicCAS(lock,0,1) / atomicExch(lock,0); group_runtime.hpp:190-205).
+__device__ __forceinline__ void lock_acquire(uint32_t* lock) {
+  const uint64_t t0 = globaltimer_ns();
+  while (atomicCAS(lock, 0u, 1u) != 0u) {
+    __nanosleep(32);
+    if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
+  }
+  __threadfence();
+}
+__device__ __forceinline__ void lock_release(uint32_t* lock) {
+  __threadfence();  // Alg. 3 line 5: publish the record before the release
+  atomicExch(lock, 0u);
+}
+
+// ------------------------------------------------------ classic phase 1
+// One particle per lane, block = group_size lanes (engine_reduction.hpp:33-36,
+// engine_queue.hpp:39-58 / 86-104). Dynamic smem: padded doubles + padded u32.
+template <int F, int MODE>
+__global__ void k_classic_step(KParams P, KState S, KCtl C, uint32_t t, uint32_t padded) {
+  extern __shared__ double smem_d[];
+  double* wf = smem_d;
+  uint32_t* wi = reinterpret_cast<uint32_t*>(wf + padded);
+  __shared__ uint32_t s_n;
+  const uint32_t lane = threadIdx.x;
+  const uint32_t g = blockIdx.x;
+  const uint32_t li = g * P.gs + lane;
+  const bool active = li < P.n;
+  if (MODE == kQueue || MODE == kQueueLock) {
+    if (lane == 0) s_n = 0;
+    __syncthreads();
+  }
+  double fit = -INFINITY;
+  if (active) fit = advance_one<F>(P, S, t, li, C.snap_pos);
+
+  if (MODE == kTree || MODE == kTreeUnrolled) {
+    wf[lane] = active ? fit : -INFINITY;  // inactive lanes hold the sentinel
+    wi[lane] = active ? P.base + li : kNoParticle;
+    for (uint32_t pad = lane + P.gs; pad < padded; pad += P.gs) {
+      wf[pad] = -INFINITY;
+      wi[pad] = kNoParticle;
+    }
+    __syncthreads();
+    if (MODE == kTreeUnrolled)
+      tree_unrolled(wf, wi, lane, padded);
+    else
+      tree_looped(wf, wi, lane, padded);
+    if (lane == 0) {
+      C.aux_fit[g] = wf[0];
+      C.aux_idx[g] = wi[0];
+    }
+  } else {
+    const double snap_fit = C.snap->fit;
+    if (active && fit > snap_fit) {  // Alg. 2 lines 1-4: conditional atomic append
+      const uint32_t slot = atomicAdd(&s_n, 1u);
+      wf[slot] = fit;
+      wi[slot] = P.base + li;
+    }
+    __syncthreads();
+    if (lane == 0) {
+      const uint32_t n = s_n;
+      double bf = -INFINITY;
+      uint32_t bi = kNoParticle;
+      if (n != 0) {  // scan_queue (engine_queue.hpp:28-35): sequential leader scan
+        bf = wf[0];
+        bi = wi[0];
+        for (uint32_t j = 1; j < n; ++j)
+          if (beats(wf[j], wi[j], bf, bi)) {
+            bf = wf[j];
+            bi = wi[j];
+          }
+        atomicAdd(&C.admitted[t], static_cast<unsigned long long>(n));
+      }
+      if (MODE == kQueue) {
+        C.aux_fit[g] = bf;
+        C.aux_idx[g] = bi;
+      } else {  // queue-lock: lock-guarded beats() commit into the live record
+        if (n != 0) {
+          lock_acquire(C.lock);
+          const double lf = *reinterpret_cast<volatile double*>(&C.live->fit);
+          const uint32_t lp = *reinterpret_cast<volatile uint32_t*>(&C.live->particle);
+          if (beats(bf, bi, lf, lp)) {
+            C.live->fit = bf;
+            C.live->particle = bi;
+            for (uint32_t a = 0; a < P.d; ++a)
+              C.live_pos[a] = S.pos[static_cast<size_t>(a) * P.ld + (bi - P.base)];
+          }
+          lock_release(C.lock);
+        }
+        // last block to finish publishes live -> snapshot and the trace entry
+        __threadfence();
+        if (atomicAdd(C.ticket, 1u) == gridDim.x - 1) {
+          __threadfence();
+          const double lf = *reinterpret_cast<volatile double*>(&C.live->fit);
+          const uint32_t lp = *reinterpret_cast<volatile uint32_t*>(&C.live->particle);
+          if (lp != C.snap->particle || lf != C.snap->fit) {
+            for (uint32_t a = 0; a < P.d; ++a)
+              C.snap_pos[a] = *reinterpret_cast<volatile double*>(&C.live_pos[a]);
+            C.snap->fit = lf;
+            C.snap->particle = lp;
+          }
+          C.trace[t] = lf;
+          C.trace_idx[t] = lp;
+          *C.ticket = 0;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------ classic phase 2
+// One group folds the aux slots (engine_reduction.hpp:29-32, engine_queue.hpp:63-78)
+// and adopts the winner under a strict > against the record, gathering the
+// position by index (adopt_record, engine.hpp:57-62).
+template <int MODE>
+__global__ void k_classic_fold(KParams P, KState S, KCtl C, uint32_t t, uint32_t groups,
+                               uint32_t padded) {
+  extern __shared__ double smem_d[];
+  double* wf = smem_d;
+  uint32_t* wi = reinterpret_cast<uint32_t*>(wf + padded);
+  __shared__ uint32_t s_n;
+  __shared__ double s_wf;
+  __shared__ uint32_t s_wi;
+  __shared__ int s_adopt;
+  const uint32_t lane = threadIdx.x;
+  double mf = -INFINITY;
+  uint32_t mi = kNoParticle;
+  for (uint32_t k = lane; k < groups; k += P.gs)
+    if (beats(C.aux_fit[k], C.aux_idx[k], mf, mi)) {
+      mf = C.aux_fit[k];
+      mi = C.aux_idx[k];
+    }
+  const double snap_fit = C.snap->fit;
+  if (MODE == kTree || MODE == kTreeUnrolled) {
+    wf[lane] = mf;
+    wi[lane] = mi;
+    for (uint32_t pad = lane + P.gs; pad < padded; pad += P.gs) {
+      wf[pad] = -INFINITY;
+      wi[pad] = kNoParticle;
+    }
+    __syncthreads();
+    if (MODE == kTreeUnrolled)
+      tree_unrolled(wf, wi, lane, padded);
+    else
+      tree_looped(wf, wi, lane, padded);
+    if (lane == 0) {
+      s_wf = wf[0];
+      s_wi = wi[0];
+      s_adopt = wf[0] > snap_fit;
+    }
+  } else {
+    if (lane == 0) s_n = 0;
+    __syncthreads();
+    if (mf > snap_fit) {
+      const uint32_t slot = atomicAdd(&s_n, 1u);
+      wf[slot] = mf;
+      wi[slot] = mi;
+    }
+    __syncthreads();
+    if (lane == 0) {
+      const uint32_t n = s_n;
+      s_adopt = 0;
+      if (n != 0) {
+        double bf = wf[0];
+        uint32_t bi = wi[0];
+        for (uint32_t j = 1; j < n; ++j)
+          if (beats(wf[j], wi[j], bf, bi)) {
+            bf = wf[j];
+            bi = wi[j];
+          }
+        s_wf = bf;
+        s_wi = bi;
+        s_adopt = bf > snap_fit;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_adopt) {
+    const uint32_t w = s_wi;
+    for (uint32_t a = lane; a < P.d; a += blockDim.x)
+      C.snap_pos[a] = S.pos[static_cast<size_t>(a) * P.ld + (w - P.base)];
+    if (lane == 0) {
+      C.snap->fit = s_wf;
+      C.snap->particle = w;
+    }
+  }
+  if (lane == 0) {
+    C.trace[t] = s_adopt ? s_wf : snap_fit;
+    C.trace_idx[t] = s_adopt ? s_wi : C.snap->particle;
+  }
+}
+
+// ---------------------------------------------------- shared block logic
+// Per-thread candidate over the thread's pairs -> block queue in smem via
+// warp ballot + shuffle argmax (one append per warp with a candidate).
+struct BlockCand {
+  double f[kSyncWarps];
+  uint32_t i[kSyncWarps];
+  uint32_t s[kSyncWarps];
+  uint32_t n;
+  unsigned long long adm;
+};
+
+__device__ __forceinline__ void warp_publish(BlockCand& bc, double bf, uint32_t bi, uint32_t adm) {
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, bi != kNoParticle);
+  const uint32_t wadm = __reduce_add_sync(0xffffffffu, adm);
+  if (m) {
+    warp_argmax(bf, bi);
+    if (lane == 0) {
+      const uint32_t slot = atomicAdd(&bc.n, 1u);
+      bc.f[slot] = bf;
+      bc.i[slot] = bi;
+    }
+  }
+  if (lane == 0 && wadm) atomicAdd(&bc.adm, static_cast<unsigned long long>(wadm));
+}
+
+// Thread's share of the fused step over pairs [p_begin, p_end) of this block.
+template <int F>
+__device__ __forceinline__ void step_pairs(const KParams& P, const KState& S, uint32_t t,
+                                           uint32_t p_begin, uint32_t p_end,
+                                           const double* gpos, double snap_fit, double& bf,
+                                           uint32_t& bi, uint32_t& adm) {
+  bf = -INFINITY;
+  bi = kNoParticle;
+  adm = 0;
+  for (uint32_t p = p_begin + threadIdx.x; p < p_end; p += blockDim.x) {
+    const uint32_t li = 2 * p;
+    double fa, fb;
+    advance_pair<F>(P, S, t, li, gpos, fa, fb);
+    if (fa > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+      ++adm;
+      if (beats(fa, P.base + li, bf, bi)) {
+        bf = fa;
+        bi = P.base + li;
+      }
+    }
+    if (li + 1 < P.n && fb > snap_fit) {
+      ++adm;
+      if (beats(fb, P.base + li + 1, bf, bi)) {
+        bf = fb;
+        bi = P.base + li + 1;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void block_pair_range(const KParams& P, uint32_t& b, uint32_t& e) {
+  const uint64_t pairs = (P.n + 1ull) / 2;
+  b = static_cast<uint32_t>(pairs * blockIdx.x / gridDim.x);
+  e = static_cast<uint32_t>(pairs * (blockIdx.x + 1) / gridDim.x);
+}
+
+// --------------------------------------------------------- sync (fused)
+template <int F>
+__global__ void __launch_bounds__(kSyncThreads) k_sync(KParams P, KState S, KCtl C, uint32_t t0,
+                                                       uint32_t t1) {
+  extern __shared__ double s_gpos[];  // [d] iteration-start gbest position
+  __shared__ BlockCand bc;
+  __shared__ double s_rf[kSyncWarps];
+  __shared__ uint32_t s_ri[kSyncWarps], s_rs[kSyncWarps];
+  __shared__ double s_snap_fit;
+  __shared__ uint32_t s_snap_idx, s_win_slot;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  if (tid == 0) {
+    s_snap_fit = C.snap->fit;
+    s_snap_idx = C.snap->particle;
+    bc.n = 0;
+    bc.adm = 0;
+  }
+  __syncthreads();
+  double snap_fit = s_snap_fit;
+  uint32_t snap_idx = s_snap_idx;
+  uint32_t p_begin, p_end;
+  block_pair_range(P, p_begin, p_end);
+  const uint32_t cap = C.q_cap;
+  uint32_t bar_target = 0;
+
+  for (uint32_t t = t0; t < t1; ++t) {
+    const uint32_t qb = t % 3;
+    double bf;
+    uint32_t bi, adm;
+    step_pairs<F>(P, S, t, p_begin, p_end, s_gpos, snap_fit, bf, bi, adm);
+    warp_publish(bc, bf, bi, adm);
+    __syncthreads();
+
+    if (warp == 0) {  // block winner -> grid queue; then the grid barrier
+      const uint32_t nq = bc.n;
+      if (nq) {
+        double f = lane < nq ? bc.f[lane] : -INFINITY;
+        uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
+        warp_argmax(f, i);
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(&C.q_count[qb], 1u);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        const size_t e = static_cast<size_t>(qb) * cap + slot;
+        if (lane == 0) {
+          C.q_fit[e] = f;
+          C.q_idx[e] = i;
+        }
+        for (uint32_t a = lane; a < P.d; a += 32)
+          C.q_pos[e * P.d + a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
+      }
+      if (lane == 0) {
+        if (bc.adm) atomicAdd(&C.admitted[t], bc.adm);
+        if (blockIdx.x == 0) C.q_count[(t + 1) % 3] = 0;  // last read two barriers ago
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        bar_target += gridDim.x;
+        red_release_gpu_add(C.bar, 1u);
+        const uint64_t ts = globaltimer_ns();
+        while (ld_acquire_gpu(C.bar) < bar_target) {
+          if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+        }
+        __threadfence();
+      }
+    }
+    __syncthreads();
+
+    // resolve: every block reduces the grid queue itself (deterministic)
+    const uint32_t nq = __ldcg(&C.q_count[qb]);
+    if (nq) {
+      double f = -INFINITY;
+      uint32_t i = kNoParticle, s = 0;
+      for (uint32_t k = tid; k < nq; k += blockDim.x) {
+        const size_t e = static_cast<size_t>(qb) * cap + k;
+        const double ef = __ldcg(&C.q_fit[e]);
+        const uint32_t ei = __ldcg(&C.q_idx[e]);
+        if (beats(ef, ei, f, i)) {
+          f = ef;
+          i = ei;
+          s = k;
+        }
+      }
+      warp_argmax3(f, i, s);
+      if (lane == 0) {
+        s_rf[warp] = f;
+        s_ri[warp] = i;
+        s_rs[warp] = s;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        f = lane < kSyncWarps ? s_rf[lane] : -INFINITY;
+        i = lane < kSyncWarps ? s_ri[lane] : kNoParticle;
+        s = lane < kSyncWarps ? s_rs[lane] : 0;
+        warp_argmax3(f, i, s);
+        if (lane == 0) {  // every entry passed fit > snap_fit, so the winner is adopted
+          s_snap_fit = f;
+          s_snap_idx = i;
+          s_win_slot = s;
+        }
+      }
+      __syncthreads();
+      snap_fit = s_snap_fit;
+      snap_idx = s_snap_idx;
+      const size_t e = static_cast<size_t>(qb) * cap + s_win_slot;
+      for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.q_pos[e * P.d + a]);
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      C.trace[t] = snap_fit;
+      C.trace_idx[t] = snap_idx;
+    }
+    if (tid == 0) {
+      bc.n = 0;
+      bc.adm = 0;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0) {
+    for (uint32_t a = tid; a < P.d; a += blockDim.x) {
+      C.snap_pos[a] = s_gpos[a];
+      C.live_pos[a] = s_gpos[a];
+    }
+    if (tid == 0) {
+      const Rec r{snap_fit, snap_idx, 0u};
+      *C.snap = r;
+      *C.live = r;
+    }
+  }
+}
+
+// ------------------------------------------------------- shard propose
+// One iteration of the fused step on a shard; the last block to finish
+// reduces the grid queue to the shard's candidate record
+// {fit, particle, admitted, pos[d]} (sentinel when nothing was admitted).
+template <int F>
+__global__ void __launch_bounds__(kSyncThreads) k_propose(KParams P, KState S, KCtl C, uint32_t t,
+                                                          unsigned char* record) {
+  extern __shared__ double s_gpos[];
+  __shared__ BlockCand bc;
+  __shared__ double s_rf[kSyncWarps];
+  __shared__ uint32_t s_ri[kSyncWarps], s_rs[kSyncWarps];
+  __shared__ int s_last;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  if (tid == 0) {
+    bc.n = 0;
+    bc.adm = 0;
+  }
+  __syncthreads();
+  const double snap_fit = C.snap->fit;
+  uint32_t p_begin, p_end;
+  block_pair_range(P, p_begin, p_end);
+  double bf;
+  uint32_t bi, adm;
+  step_pairs<F>(P, S, t, p_begin, p_end, s_gpos, snap_fit, bf, bi, adm);
+  warp_publish(bc, bf, bi, adm);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nq = bc.n;
+    if (nq) {
+      double f = lane < nq ? bc.f[lane] : -INFINITY;
+      uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
+      warp_argmax(f, i);
+      uint32_t slot = 0;
+      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (lane == 0) {
+        C.q_fit[slot] = f;
+        C.q_idx[slot] = i;
+      }
+      for (uint32_t a = lane; a < P.d; a += 32)
+        C.q_pos[static_cast<size_t>(slot) * P.d + a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
+    }
+    if (lane == 0 && bc.adm) atomicAdd(&C.admitted[t], bc.adm);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) s_last = atomicAdd(C.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const uint32_t nq = __ldcg(&C.q_count[0]);
+  double f = -INFINITY;
+  uint32_t i = kNoParticle, s = 0;
+  for (uint32_t k = tid; k < nq; k += blockDim.x) {
+    const double ef = __ldcg(&C.q_fit[k]);
+    const uint32_t ei = __ldcg(&C.q_idx[k]);
+    if (beats(ef, ei, f, i)) {
+      f = ef;
+      i = ei;
+      s = k;
+    }
+  }
+  warp_argmax3(f, i, s);
+  if (lane == 0) {
+    s_rf[warp] = f;
+    s_ri[warp] = i;
+    s_rs[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    f = lane < kSyncWarps ? s_rf[lane] : -INFINITY;
+    i = lane < kSyncWarps ? s_ri[lane] : kNoParticle;
+    s = lane < kSyncWarps ? s_rs[lane] : 0;
+    warp_argmax3(f, i, s);
+    if (lane == 0) {
+      s_rf[0] = f;
+      s_ri[0] = i;
+      s_rs[0] = s;
+    }
+  }
+  __syncthreads();
+  Rec* rec = reinterpret_cast<Rec*>(record);
+  double* rpos = reinterpret_cast<double*>(record + sizeof(Rec));
+  for (uint32_t a = tid; a < P.d; a += blockDim.x)
+    rpos[a] = nq ? __ldcg(&C.q_pos[static_cast<size_t>(s_rs[0]) * P.d + a]) : 0.0;
+  if (tid == 0) {
+    const unsigned long long am = *reinterpret_cast<volatile unsigned long long*>(&C.admitted[t]);
+    rec->fit = nq ? s_rf[0] : -INFINITY;
+    rec->particle = nq ? s_ri[0] : kNoParticle;
+    rec->admitted = static_cast<uint32_t>(am);
+    C.q_count[0] = 0;
+    *C.ticket = 0;
+  }
+}
+
+// All shards apply the same selection: beats() among records, strict > vs snapshot.
+__global__ void k_commit(KParams P, KCtl C, uint32_t t, const unsigned char* records, uint32_t nrec,
+                         size_t rec_bytes, int count_admitted) {
+  __shared__ int s_w;
+  if (threadIdx.x == 0) {
+    double bf = -INFINITY;
+    uint32_t bi = kNoParticle;
+    int w = -1;
+    unsigned long long adm = 0;
+    for (uint32_t r = 0; r < nrec; ++r) {
+      const Rec* rec = reinterpret_cast<const Rec*>(records + r * rec_bytes);
+      adm += rec->admitted;
+      if (rec->particle != kNoParticle && beats(rec->fit, rec->particle, bf, bi)) {
+        bf = rec->fit;
+        bi = rec->particle;
+        w = static_cast<int>(r);
+      }
+    }
+    if (!(w >= 0 && bf > C.snap->fit)) w = -1;
+    s_w = w;
+    if (w >= 0) {
+      C.snap->fit = bf;
+      C.snap->particle = bi;
+    }
+    if (count_admitted) C.admitted[t] = adm;
+    C.trace[t] = C.snap->fit;
+    C.trace_idx[t] = C.snap->particle;
+  }
+  __syncthreads();
+  if (s_w >= 0) {
+    const double* rpos = reinterpret_cast<const double*>(records + s_w * rec_bytes + sizeof(Rec));
+    for (uint32_t a = threadIdx.x; a < P.d; a += blockDim.x) C.snap_pos[a] = rpos[a];
+  }
+}
+
+// ---------------------------------------------------------------- async
+// Free-running blocks. The live record {fit, particle, pos[d]} is guarded by
+// a seqlock: readers retry on an odd or changed version; a writer takes the
+// record with CAS(version: even -> odd), re-checks beats() under it, writes,
+// and releases with version+2. No grid barrier anywhere.
+template <int F>
+__global__ void __launch_bounds__(kSyncThreads) k_async(KParams P, KState S, KCtl C, uint32_t t0,
+                                                        uint32_t t1) {
+  extern __shared__ double s_gpos[];
+  __shared__ BlockCand bc;
+  __shared__ double s_fit;
+  __shared__ uint32_t s_idx, s_ver, s_have, s_ok;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t p_begin, p_end;
+  block_pair_range(P, p_begin, p_end);
+  if (tid == 0) {
+    s_have = 0;
+    s_ver = 0xffffffffu;
+    bc.n = 0;
+    bc.adm = 0;
+  }
+  __syncthreads();
+  for (uint32_t t = t0; t < t1; ++t) {
+    // consistent read of the live record (skip the position copy when unchanged)
+    const uint64_t ts = globaltimer_ns();
+    for (;;) {
+      __syncthreads();  // previous round's readers are done with s_ok / s_have
+      if (tid == 0) {
+        const uint32_t v = ld_acquire_gpu(C.seq);
+        s_ok = (v & 1u) == 0u;
+        s_have = 1;  // unchanged since our last copy
+        if (s_ok && v != s_ver) {
+          s_have = 2;  // needs a copy
+          s_ver = v;
+        }
+        if (!s_ok && globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+      }
+      __syncthreads();
+      if (!s_ok) continue;
+      if (s_have == 1) break;
+      for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.live_pos[a]);
+      if (tid == 0) {
+        s_fit = __ldcg(&C.live->fit);
+        s_idx = __ldcg(&C.live->particle);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        const uint32_t v2 = ld_acquire_gpu(C.seq);
+        s_ok = v2 == s_ver;
+        if (!s_ok) s_ver = 0xffffffffu;
+      }
+      __syncthreads();
+      if (s_ok) break;
+    }
+    const double snap_fit = s_fit;
+    double bf;
+    uint32_t bi, adm;
+    step_pairs<F>(P, S, t, p_begin, p_end, s_gpos, snap_fit, bf, bi, adm);
+    warp_publish(bc, bf, bi, adm);
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t nq = bc.n;
+      double view = snap_fit;
+      if (nq) {
+        double f = lane < nq ? bc.f[lane] : -INFINITY;
+        uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
+        warp_argmax(f, i);
+        // cheap pre-check against the live fit; re-checked under the CAS
+        const double lf0 = __ldcg(&C.live->fit);
+        const uint32_t lp0 = __ldcg(&C.live->particle);
+        if (beats(f, i, lf0, lp0)) {
+          uint32_t v = 0;
+          if (lane == 0) {
+            const uint64_t tl = globaltimer_ns();
+            for (;;) {
+              v = ld_acquire_gpu(C.seq);
+              if (!(v & 1u) && atomicCAS(C.seq, v, v + 1u) == v) break;
+              if (globaltimer_ns() - tl > kSpinTimeoutNs) __trap();
+            }
+            __threadfence();
+          }
+          v = __shfl_sync(0xffffffffu, v, 0);
+          const double lf = __ldcg(&C.live->fit);
+          const uint32_t lp = __ldcg(&C.live->particle);
+          const bool win = beats(f, i, lf, lp);
+          if (win) {
+            for (uint32_t a = lane; a < P.d; a += 32)
+              C.live_pos[a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
+            if (lane == 0) {
+              C.live->fit = f;
+              C.live->particle = i;
+            }
+            view = f;
+          } else {
+            view = lf;
+          }
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release_gpu(C.seq, v + 2u);
+        } else {
+          view = lf0 > view ? lf0 : view;
+        }
+      }
+      if (lane == 0) {
+        if (bc.adm) atomicAdd(&C.admitted[t], bc.adm);
+        atomicMax(&C.trace_key[t], order_key(view));
+        bc.n = 0;
+        bc.adm = 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace cupso
