@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py -- particle-updates/sec of the B200-native PSO step (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg3|cfg4|cfg5] [--variant cuda-sync]
+
+One bench "step" = one full optimisation run of the workload's T iterations
+(init_swarm excluded, exactly like the reference's compute_seconds,
+engine_serial.hpp:25-40), with the swarm resident in HBM. The default
+workload is BASELINE.json configs[1]: 1-D cubic, 2^20 particles, 1000
+iterations, synchronous atomic variant (cuda-sync); the in-repo reduction
+baseline kernel (cuda-reduction) is timed on the same workload in the same run.
+
+value   = particles * iterations * steps * world / max-over-ranks device seconds
+e2e     = the same metric through the reference-facing C-ABI call cupso_run
+          (host params in, host trace/gbest out, allocation + init + H2D/D2H
+          inside the timed region), wall clock
+roofline: algorithmic bytes (5d+1)*8 per particle-update per
+          launch / CUDA-event duration of that launch, against MEASURED_PEAKS.json
+cpu_baseline: the unmodified reference (oracle/_ref, queue-lock engine, all
+          host threads) on a bounded sample of the same workload, rank 0 only
+Multi-GPU (torchrun): weak scaling, each rank holds a contiguous shard of one
+swarm of world*N particles; the per-iteration gbest exchange is an NCCL
+all-gather of one (16+8d)-byte record per rank issued by libcupso on its stream.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (fitness, particles, dims, iters, default variant, description)
+    "cfg2": ("cubic", 1 << 20, 1, 1000, "cuda-sync", "BASELINE configs[1]: 1-D cubic, 2^20 particles, 1000 iterations"),
+    "cfg3": ("cubic", 1 << 24, 1, 100, "cuda-async", "BASELINE configs[2]: 1-D cubic, 2^24 particles, async persistent"),
+    "cfg4": ("rastrigin", 1 << 20, 32, 100, "cuda-sync", "BASELINE configs[3]: Rastrigin d=32, 2^20 particles"),
+    "cfg5": ("sphere", 1 << 28, 8, 20, "cuda-sync", "BASELINE configs[4]: sphere d=8, 2^28 particles (per GPU: 2^28/N)"),
+}
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak_gbs():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload: str, variant: str):
+    """dram bytes per launch from the committed ncu summary, or None."""
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
+            os.path.join(ROOT, "profiles")) else []:
+        if name.startswith("ncu_summary") and name.endswith(".json"):
+            try:
+                with open(os.path.join(ROOT, "profiles", name)) as fh:
+                    d = json.load(fh)
+                e = d.get(workload, {}).get(variant)
+                if e and e.get("dram_bytes_per_launch") is not None:
+                    return e["dram_bytes_per_launch"], e.get("iters_per_launch")
+            except Exception:
+                pass
+    return None, None
+
+
+def cpu_reference_leg(fitness, n, d, max_seconds=12.0, sample_iters=None):
+    """The unmodified reference (oracle/_ref) queue-lock engine on all host threads,
+    timed on a bounded sample of the workload. Checker/baseline only."""
+    import oracle as orc
+    if not os.path.exists(orc.REF_SO):
+        if os.path.isdir(orc.REF_INC):
+            orc.build(ref=True)
+    if os.path.exists(orc.REF_SO):
+        kind = "reference"
+        ref = orc.Reference()
+        threads = os.cpu_count() or 1
+        # calibrate: 2 iterations, then size the sample to ~max_seconds
+        r, _ = ref.run("queue-lock", fitness, n, d, 2, 1, threads=threads, want_particles=False)
+        per_iter = max(r.compute_seconds / 2, 1e-6)
+        iters = sample_iters or max(2, min(1000, int(max_seconds / per_iter)))
+        r, _ = ref.run("queue-lock", fitness, n, d, iters, 1, threads=threads, want_particles=False)
+        secs = r.compute_seconds
+        engine = "queue-lock"
+    else:  # the C restatement, single thread
+        kind = "port"
+        o = orc.Oracle()
+        threads = 1
+        r = o.run_serial(fitness, n, d, 2, 1, want_state=False)
+        per_iter = max(r.compute_seconds / 2, 1e-6)
+        iters = sample_iters or max(2, min(1000, int(max_seconds / per_iter)))
+        r = o.run_serial(fitness, n, d, iters, 1, want_state=False)
+        secs = r.compute_seconds
+        engine = "serial (oracle/pso_oracle.c)"
+    return {"value": n * iters / secs, "unit": "particle-updates/s", "cores": threads, "kind": kind,
+            "sample": f"{engine}: {fitness} d={d}, {n} particles x {iters} iterations "
+                      f"(compute loop {secs:.2f} s, seed 1, cpu={_cpu_model()})"}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    fitness, n, d, T, _, desc = WORKLOADS[args.workload]
+    n_rank = n if args.workload != "cfg5" else (1 << 24)  # 2^28 FP64 state does not fit host RAM budget
+    import oracle as orc
+    if not os.path.exists(orc.REF_SO) and os.path.isdir(orc.REF_INC):
+        orc.build(ref=True)
+    base = cpu_reference_leg(fitness, n_rank, d, max_seconds=3.0)
+    # each step: a bounded sample run of the same workload
+    iters = int(base["sample"].split(" x ")[1].split(" ")[0])
+    vals = []
+    if base["kind"] == "reference":
+        ref = orc.Reference()
+        for k in range(args.warmup + args.steps):
+            r, _ = ref.run("queue-lock", fitness, n_rank, d, iters, 1, threads=base["cores"], want_particles=False)
+            if k >= args.warmup:
+                vals.append(r.compute_seconds)
+    else:
+        o = orc.Oracle()
+        for k in range(args.warmup + args.steps):
+            r = o.run_serial(fitness, n_rank, d, iters, 1, want_state=False)
+            if k >= args.warmup:
+                vals.append(r.compute_seconds)
+    secs = sum(vals)
+    value = n_rank * iters * len(vals) / secs
+    line = {
+        "impl": "reference", "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / len(vals), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox init of the reference)",
+        "config": {"workload": desc, "fitness": fitness, "particles": n_rank, "dims": d,
+                   "iterations_per_step": iters, "engine": "reference queue-lock (all host threads)"},
+        "cpu_baseline": {**base, "value": value},
+        "e2e": {"value": value, "unit": "particle-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def flush_l2(torch, dev):
+    buf = getattr(flush_l2, "buf", None)
+    if buf is None:
+        buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+        flush_l2.buf = buf
+    buf.random_(0, 1 << 30)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-baseline-kernel", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import torch
+    import paper_2205_01313_b200 as cp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    fitness, n_per_rank, d, T, default_variant, desc = WORKLOADS[args.workload]
+    if args.workload == "cfg5":
+        n_total = n_per_rank
+        n_per_rank = n_total // world
+    else:
+        n_total = n_per_rank * world
+    if args.iters:
+        T = args.iters
+    variant_name = args.variant or default_variant
+    engine = cp.find_engine(variant_name)
+    f = cp.find_fitness(fitness)
+    p = cp.make_params(f, n_total, d, T)
+    seed = 1
+
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://", world_size=world, rank=rank)
+        pg = dist
+    first, count = cp.shard_range(n_total, world, rank)
+
+    def barrier():
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    sw = cp.Swarm(p, f, seed, device=local, first=first, count=count)
+    if world > 1:
+        uid = [cp.nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(uid, src=0)
+        sw.nccl_init(uid[0], world, rank)
+
+    # ---- W warmup steps, then exactly K timed steps. Each step: init_swarm and an
+    # L2 flush (untimed), then the T iterations timed with CUDA events recorded by
+    # libcupso on the stream that launches the kernels (device seconds). ----
+    for k in range(args.warmup):
+        sw.init()
+        flush_l2(torch, dev)
+        barrier()
+        sw.step(engine.variant, T)
+    per_step = []
+    barrier()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            sw.init()
+            flush_l2(torch, dev)
+            barrier()
+            per_step.append(sw.step(engine.variant, T))
+        barrier()
+    clocks = clk.summary()
+    dev_secs = sum(per_step)
+    if pg:
+        t = torch.tensor([dev_secs], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        dev_secs = float(t.item())
+    K = len(per_step)
+    value = n_total * T * K / dev_secs
+    gb = sw.gbest()
+    grid = sw.sync_grid_blocks()
+
+    # ---- roofline of the dominant kernel (one launch = T iterations for the persistent kernels) ----
+    bytes_per_pu = (5 * d + 1) * 8
+    launches_per_step = {"cuda-sync": 1 if world == 1 else 2 * T, "cuda-async": 1,
+                         "cuda-queue-lock": T, "cuda-queue": 2 * T, "cuda-reduction": 2 * T,
+                         "cuda-unrolled": 2 * T}[variant_name]
+    iters_per_launch = T if variant_name in ("cuda-sync", "cuda-async") and world == 1 else 1
+    launch_secs = (dev_secs / K) / (T / iters_per_launch)
+    alg_bytes = count * iters_per_launch * bytes_per_pu
+    peak, peak_src = measured_peak_gbs()
+    achieved = alg_bytes / launch_secs / 1e9
+    traffic, traffic_iters = ncu_traffic(args.workload, variant_name)
+    if traffic is not None and traffic_iters:
+        traffic = traffic * iters_per_launch / traffic_iters
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "kernel": f"k_sync<{fitness}>" if variant_name == "cuda-sync" else variant_name,
+                "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
+                "bytes_per_particle_update": bytes_per_pu}
+
+    extra = {}
+    # ---- the in-repo reduction baseline kernel on the same workload (rank 0, N=1) ----
+    if world == 1 and not args.no_baseline_kernel and variant_name != "cuda-reduction":
+        red = cp.find_engine("cuda-reduction")
+        rs = []
+        for k in range(2 + max(2, args.steps // 2)):
+            sw.init()
+            flush_l2(torch, dev)
+            torch.cuda.synchronize()
+            s = sw.step(red.variant, T)
+            if k >= 2:
+                rs.append(s)
+        rv = n_total * T * len(rs) / sum(rs)
+        extra["reduction_baseline"] = {"variant": "cuda-reduction", "value": rv, "unit": "particle-updates/s",
+                                       "speedup_of_headline": value / rv}
+
+    # ---- e2e through the reference-facing C-ABI call (cupso_run), host buffers ----
+    e2e = None
+    if world == 1:
+        e2e_secs = []
+        for k in range(1 + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = engine.run(p, f, cp.rng_key(seed), cp.exec_options(device=local))
+            e2e_secs.append(time.perf_counter() - t0)
+        e2e_secs = e2e_secs[1:]
+        h2d = C.sizeof(cp._lib.cupso_params) + 8  # params + seed; the swarm is initialised on device
+        d2h = T * (8 + 4 + 8 + 8 + 8) + (16 + 8 * d) + 16  # trace, particle, admitted, trace_key, cummax; gbest; initial
+        e2e = {"value": n_total * T * len(e2e_secs) / sum(e2e_secs), "unit": "particle-updates/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "cupso_run via find_engine(...).run (alloc + init_swarm + T iterations + result D2H)",
+               "final_gbest_fit": r.gbest_fit}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_leg(fitness, min(n_per_rank, 1 << 24), d)
+        except Exception as e:  # the baseline is reported, never the target
+            cpu = {"value": None, "unit": "particle-updates/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * dev_secs / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Philox-initialised swarm, reference make_params defaults)",
+            "config": {"workload": desc, "fitness": fitness, "particles_total": n_total,
+                       "particles_per_gpu": count, "dims": d, "iterations_per_step": T,
+                       "variant": variant_name, "parallelism": f"dp{world} (particle shards)",
+                       "sync_grid_blocks": grid,
+                       "l2": "flushed (512 MiB write) before every step; within a step the swarm stays resident as in a real run"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches_per_step * K, "final_gbest_fit": gb.fit,
+            **extra,
+        }
+        print(json.dumps(line), flush=True)
+    sw.close()
+    if pg:
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

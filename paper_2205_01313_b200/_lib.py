@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libcupso.so")
+LIB_PATH = os.environ.get("CUPSO_LIB") or os.path.join(PKG_DIR, "libcupso.so")
 
 CUPSO_OK, CUPSO_EINVAL, CUPSO_ERUNTIME, CUPSO_ELOGIC, CUPSO_EDOMAIN, CUPSO_ECUDA = range(6)
 REDUCTION, UNROLLED, QUEUE, QUEUE_LOCK, SYNC, ASYNC = range(6)

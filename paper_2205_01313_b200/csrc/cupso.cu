@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -150,6 +151,7 @@ struct cupso_swarm {
   double* eval_buf = nullptr;           // fitness export scratch
   uint32_t groups = 0;
   int sync_grid = 0;
+  int step_cfg = 0;
   uint32_t q_alloc = 0;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
   std::vector<uint8_t> is_async;
@@ -182,6 +184,36 @@ cupso_status dispatch_fit(int fid, Fn&& fn) {
   return CUPSO_OK;
 }
 
+// Fused-step tunings (particles per thread, prefetch, min blocks per SM).
+using Cfg0 = StepCfg<2, 0, 5>;
+using Cfg1 = StepCfg<2, 1, 3>;
+using Cfg2 = StepCfg<1, 0, 8>;
+using Cfg3 = StepCfg<1, 1, 6>;
+using Cfg4 = StepCfg<2, 0, 6>;
+using Cfg5 = StepCfg<1, 0, 6>;
+constexpr int kNumCfg = 6;
+
+template <typename Fn>
+void dispatch_cfg(int c, Fn&& fn) {
+  switch (c) {
+    case 0: fn(Cfg0{}); break;
+    case 1: fn(Cfg1{}); break;
+    case 2: fn(Cfg2{}); break;
+    case 3: fn(Cfg3{}); break;
+    case 4: fn(Cfg4{}); break;
+    default: fn(Cfg5{}); break;
+  }
+}
+
+int default_step_cfg(const KParams& P) {
+  if (const char* e = getenv("CUPSO_STEP_CFG")) {
+    const int c = atoi(e);
+    if (c >= 0 && c < kNumCfg) return c;
+  }
+  (void)P;
+  return 0;
+}
+
 void key_schedule(uint64_t seed, KParams& P) {
   uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
   for (int r = 0; r < 10; ++r) {
@@ -208,26 +240,31 @@ cupso_status ensure_sync_grid(cupso_swarm* h) {
     return fail(CUPSO_EINVAL, "cuda-sync/async: dims (%u) above %u", h->P.d, kMaxSyncDims);
   const size_t smem = sync_smem(h);
   int per_sm = 0;
+  int np = 1;
   cudaError_t e = cudaSuccess;
   dispatch_fit(h->fid, [&](auto F) {
     constexpr int f = decltype(F)::value;
-    if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(k_sync<f>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_async<f>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_propose<f>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
-    int a = 0, b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sync<f>, kSyncThreads, smem);
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_async<f>, kSyncThreads, smem);
-    per_sm = std::min(a, b);
+    dispatch_cfg(h->step_cfg, [&](auto CF) {
+      using Cfg = decltype(CF);
+      np = Cfg::kNP;
+      if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_sync<f, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_async<f, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_propose<f, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }
+      int a = 0, b = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sync<f, Cfg>, kSyncThreads, smem);
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_async<f, Cfg>, kSyncThreads, smem);
+      per_sm = std::min(a, b);
+    });
   });
   CK(e);
   if (per_sm < 1) return fail(CUPSO_ECUDA, "cuda-sync: kernel cannot be resident (occupancy 0)");
-  const uint64_t pairs = (h->P.n + 1ull) / 2;
+  const uint64_t units = (h->P.n + np - 1ull) / np;
   uint64_t grid = static_cast<uint64_t>(per_sm) * num_sms(h->device);
-  // keep at least ~2 pairs per thread of work per block when the swarm is small
-  const uint64_t min_work = std::max<uint64_t>(1, pairs / (2 * kSyncThreads));
+  // keep at least ~2 units per thread of work per block when the swarm is small
+  const uint64_t min_work = std::max<uint64_t>(1, units / (2 * kSyncThreads));
   grid = std::max<uint64_t>(1, std::min(grid, min_work));
   h->sync_grid = static_cast<int>(grid);
   if (h->q_alloc < grid) {
@@ -313,13 +350,16 @@ cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_
   CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
   dispatch_fit(h->fid, [&](auto F) {
     constexpr int f = decltype(F)::value;
-    void* args[] = {&h->P, &h->S, &h->C, &t0, &t1};
-    if (variant == CUPSO_SYNC)
-      e = cudaLaunchCooperativeKernel((void*)k_sync<f>, dim3(h->sync_grid), dim3(kSyncThreads), args,
-                                      smem, h->stream);
-    else
-      e = cudaLaunchCooperativeKernel((void*)k_async<f>, dim3(h->sync_grid), dim3(kSyncThreads), args,
-                                      smem, h->stream);
+    dispatch_cfg(h->step_cfg, [&](auto CF) {
+      using Cfg = decltype(CF);
+      void* args[] = {&h->P, &h->S, &h->C, &t0, &t1};
+      if (variant == CUPSO_SYNC)
+        e = cudaLaunchCooperativeKernel((void*)k_sync<f, Cfg>, dim3(h->sync_grid), dim3(kSyncThreads),
+                                        args, smem, h->stream);
+      else
+        e = cudaLaunchCooperativeKernel((void*)k_async<f, Cfg>, dim3(h->sync_grid), dim3(kSyncThreads),
+                                        args, smem, h->stream);
+    });
   });
   CK(e);
   return CUPSO_OK;
@@ -331,7 +371,10 @@ cupso_status propose_launch(cupso_swarm* h, uint32_t t, unsigned char* record_de
   cudaError_t e = cudaSuccess;
   dispatch_fit(h->fid, [&](auto F) {
     constexpr int f = decltype(F)::value;
-    k_propose<f><<<h->sync_grid, kSyncThreads, smem, h->stream>>>(h->P, h->S, h->C, t, record_dev);
+    dispatch_cfg(h->step_cfg, [&](auto CF) {
+      using Cfg = decltype(CF);
+      k_propose<f, Cfg><<<h->sync_grid, kSyncThreads, smem, h->stream>>>(h->P, h->S, h->C, t, record_dev);
+    });
     e = cudaGetLastError();
   });
   CK(e);
@@ -442,6 +485,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   P.gs = p->group_size;
   P.ld = (static_cast<uint64_t>(count) + 63) / 64 * 64;
   key_schedule(seed, P);
+  h->step_cfg = default_step_cfg(P);
   h->groups = (count + p->group_size - 1) / p->group_size;
   h->rec_bytes = sizeof(Rec) + sizeof(double) * p->dims;
   h->is_async.assign(h->T, 0);

@@ -207,52 +207,6 @@ __device__ __forceinline__ double advance_one(const KParams& P, const KState& S,
   return f;
 }
 
-// Two adjacent particles (li, li+1) per thread with 128-bit accesses: one
-// LDG.128 per array per axis covers both, and the two Philox streams give
-// the scheduler independent work. li must be even (ld is a multiple of 64).
-template <int F>
-__device__ __forceinline__ void advance_pair(const KParams& P, const KState& S, uint32_t t,
-                                             uint32_t li, const double* __restrict__ gpos,
-                                             double& fa, double& fb) {
-  const uint32_t ga = P.base + li;
-  const uint32_t gb = ga + 1;
-  Fit<F> A, B;
-  for (uint32_t a = 0; a < P.d; ++a) {
-    const size_t at = static_cast<size_t>(a) * P.ld + li;
-    const double2 x = *reinterpret_cast<const double2*>(S.pos + at);
-    const double2 v = *reinterpret_cast<const double2*>(S.vel + at);
-    const double2 pb = *reinterpret_cast<const double2*>(S.pb + at);
-    const double g = gpos[a];
-    const double r1a = uniform01(P, t, ga, a, 0);
-    const double r2a = uniform01(P, t, ga, a, 1);
-    const double r1b = uniform01(P, t, gb, a, 0);
-    const double r2b = uniform01(P, t, gb, a, 1);
-    double2 nv, nx;
-    nv.x = vel_step(P, v.x, x.x, pb.x, g, r1a, r2a);
-    nv.y = vel_step(P, v.y, x.y, pb.y, g, r1b, r2b);
-    nx.x = pos_step(P, x.x, nv.x);
-    nx.y = pos_step(P, x.y, nv.y);
-    *reinterpret_cast<double2*>(S.vel + at) = nv;
-    *reinterpret_cast<double2*>(S.pos + at) = nx;
-    A.add(nx.x, a);
-    B.add(nx.y, a);
-  }
-  fa = A.value();
-  fb = B.value();
-  const double2 pbf = *reinterpret_cast<const double2*>(S.pbf + li);
-  const bool ua = fa > pbf.x && li < P.n;
-  const bool ub = fb > pbf.y && li + 1 < P.n;
-  if (ua | ub) {  // rare after warm-up: re-read the just-written positions
-    if (ua) S.pbf[li] = fa;
-    if (ub) S.pbf[li + 1] = fb;
-    for (uint32_t a = 0; a < P.d; ++a) {
-      const size_t at = static_cast<size_t>(a) * P.ld + li;
-      if (ua) S.pb[at] = S.pos[at];
-      if (ub) S.pb[at + 1] = S.pos[at + 1];
-    }
-  }
-}
-
 // Fitness of particle li's current position (for state export / init).
 template <int F>
 __device__ __forceinline__ double eval_position(const KParams& P, const double* __restrict__ pos,

@@ -70,6 +70,32 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ double ld_acquire_gpu_f64(const double* p) {
+  double v;
+  asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Lock-free pre-check of a (fit, particle) record that only grows in beats()
+// order. Writers store particle, fence, then fit; reading fit with acquire and
+// then particle yields a particle at least as new as the fit. If the
+// candidate does not beat that pair it can never beat the live record, so
+// the caller may skip the lock; otherwise it re-checks under the lock.
+__device__ __forceinline__ bool may_beat(const Rec* r, double f, uint32_t i) {
+  const double lf = ld_acquire_gpu_f64(&r->fit);
+  const uint32_t lp = ld_relaxed_gpu(&r->particle);
+  return beats(f, i, lf, lp);
+}
+__device__ __forceinline__ void write_rec(Rec* r, double f, uint32_t i) {
+  *reinterpret_cast<volatile uint32_t*>(&r->particle) = i;
+  __threadfence();
+  *reinterpret_cast<volatile double*>(&r->fit) = f;
+}
+
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -316,15 +342,17 @@ __global__ void k_classic_step(KParams P, KState S, KCtl C, uint32_t t, uint32_t
         C.aux_fit[g] = bf;
         C.aux_idx[g] = bi;
       } else {  // queue-lock: lock-guarded beats() commit into the live record
-        if (n != 0) {
+        // Pre-check without the lock: the live record only grows in beats()
+        // order, so a leader that cannot beat it now never will. Re-checked
+        // under the lock, so the result is the reference's.
+        if (n != 0 && may_beat(C.live, bf, bi)) {
           lock_acquire(C.lock);
           const double lf = *reinterpret_cast<volatile double*>(&C.live->fit);
           const uint32_t lp = *reinterpret_cast<volatile uint32_t*>(&C.live->particle);
           if (beats(bf, bi, lf, lp)) {
-            C.live->fit = bf;
-            C.live->particle = bi;
             for (uint32_t a = 0; a < P.d; ++a)
               C.live_pos[a] = S.pos[static_cast<size_t>(a) * P.ld + (bi - P.base)];
+            write_rec(C.live, bf, bi);
           }
           lock_release(C.lock);
         }
@@ -366,11 +394,24 @@ __global__ void k_classic_fold(KParams P, KState S, KCtl C, uint32_t t, uint32_t
   const uint32_t lane = threadIdx.x;
   double mf = -INFINITY;
   uint32_t mi = kNoParticle;
-  for (uint32_t k = lane; k < groups; k += P.gs)
-    if (beats(C.aux_fit[k], C.aux_idx[k], mf, mi)) {
-      mf = C.aux_fit[k];
-      mi = C.aux_idx[k];
+  // strided fold (engine_reduction.hpp:29-32); 8 independent loads in flight per lane
+  constexpr uint32_t kBatch = 8;
+  for (uint32_t k0 = lane; k0 < groups; k0 += kBatch * P.gs) {
+    double ef[kBatch];
+    uint32_t ei[kBatch];
+#pragma unroll
+    for (uint32_t j = 0; j < kBatch; ++j) {
+      const uint32_t k = k0 + j * P.gs;
+      ef[j] = k < groups ? C.aux_fit[k] : -INFINITY;
+      ei[j] = k < groups ? C.aux_idx[k] : kNoParticle;
     }
+#pragma unroll
+    for (uint32_t j = 0; j < kBatch; ++j)
+      if (beats(ef[j], ei[j], mf, mi)) {
+        mf = ef[j];
+        mi = ei[j];
+      }
+  }
   const double snap_fit = C.snap->fit;
   if (MODE == kTree || MODE == kTreeUnrolled) {
     wf[lane] = mf;
@@ -457,45 +498,207 @@ __device__ __forceinline__ void warp_publish(BlockCand& bc, double bf, uint32_t 
   if (lane == 0 && wadm) atomicAdd(&bc.adm, static_cast<unsigned long long>(wadm));
 }
 
-// Thread's share of the fused step over pairs [p_begin, p_end) of this block.
-template <int F>
-__device__ __forceinline__ void step_pairs(const KParams& P, const KState& S, uint32_t t,
-                                           uint32_t p_begin, uint32_t p_end,
+// Tunings of the fused step: particles per thread-item (1: scalar LDG.64,
+// 2: LDG.128 over two adjacent particles), software prefetch of the next
+// item's loads, and the occupancy target handed to __launch_bounds__.
+template <int NP_, int PF_, int MINB_>
+struct StepCfg {
+  static constexpr int kNP = NP_;
+  static constexpr int kPF = PF_;
+  static constexpr int kMinBlocks = MINB_;
+};
+
+template <int NP>
+__device__ __forceinline__ void ldv(const double* p, double (&o)[NP]) {
+  if constexpr (NP == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = *p;
+  }
+}
+template <int NP>
+__device__ __forceinline__ void stv(double* p, const double (&o)[NP]) {
+  if constexpr (NP == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
+  } else {
+    *p = o[0];
+  }
+}
+
+// Thread's share of the fused step (a unit = NP adjacent particles; thread
+// (b, tid) takes units (b + k*gridDim)*blockDim + tid).
+// The thread walks its (unit, axis) items; with PF the loads of item k+1 (and
+// the next unit's pbest_fit) are issued before item k's Philox / kinematics /
+// fitness chain so the long-scoreboard wait hides behind ~115 instructions of
+// compute per particle-axis.
+template <int F, class CFG>
+__device__ __forceinline__ void step_items(const KParams& P, const KState& S, uint32_t t,
                                            const double* gpos, double snap_fit, double& bf,
                                            uint32_t& bi, uint32_t& adm) {
+  constexpr int NP = CFG::kNP;
   bf = -INFINITY;
   bi = kNoParticle;
   adm = 0;
-  for (uint32_t p = p_begin + threadIdx.x; p < p_end; p += blockDim.x) {
-    const uint32_t li = 2 * p;
-    double fa, fb;
-    advance_pair<F>(P, S, t, li, gpos, fa, fb);
-    if (fa > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
-      ++adm;
-      if (beats(fa, P.base + li, bf, bi)) {
-        bf = fa;
-        bi = P.base + li;
+  // grid-stride over units: at any moment the whole grid streams one
+  // contiguous window of every axis row (TLB / DRAM-page friendly)
+  const uint32_t u_end = (P.n + NP - 1) / NP;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= u_end) return;
+  if constexpr (!CFG::kPF) {
+    // lean nested loops (unit, axis): minimal live state -> 32 registers,
+    // full occupancy; latency is hidden by 64 resident warps per SM
+    for (; u < u_end; u += stride) {
+      const uint32_t li = NP * u;
+      const uint32_t g0 = P.base + li;
+      Fit<F> acc[NP];
+      for (uint32_t a = 0; a < P.d; ++a) {
+        const size_t at = static_cast<size_t>(a) * P.ld + li;
+        double x[NP], v[NP], pb[NP], nx[NP], nv[NP];
+        ldv<NP>(S.pos + at, x);
+        ldv<NP>(S.vel + at, v);
+        ldv<NP>(S.pb + at, pb);
+        const double g = gpos[a];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const double r1 = uniform01(P, t, g0 + k, a, 0);
+          const double r2 = uniform01(P, t, g0 + k, a, 1);
+          nv[k] = vel_step(P, v[k], x[k], pb[k], g, r1, r2);
+          nx[k] = pos_step(P, x[k], nv[k]);
+          acc[k].add(nx[k], a);
+        }
+        stv<NP>(S.vel + at, nv);
+        stv<NP>(S.pos + at, nx);
+      }
+      double pbf[NP];
+      ldv<NP>(S.pbf + li, pbf);
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const double f = acc[k].value();
+        if (k > 0 && li + k >= P.n) break;
+        if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108), rare after warm-up
+          S.pbf[li + k] = f;
+          for (uint32_t j = 0; j < P.d; ++j) {
+            const size_t aj = static_cast<size_t>(j) * P.ld + li + k;
+            S.pb[aj] = S.pos[aj];
+          }
+        }
+        if (f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+          ++adm;
+          if (beats(f, g0 + k, bf, bi)) {
+            bf = f;
+            bi = g0 + k;
+          }
+        }
       }
     }
-    if (li + 1 < P.n && fb > snap_fit) {
-      ++adm;
-      if (beats(fb, P.base + li + 1, bf, bi)) {
-        bf = fb;
-        bi = P.base + li + 1;
+    return;
+  }
+  const uint32_t d = P.d;
+  const size_t ld = P.ld;
+  uint32_t a = 0;
+  size_t at = static_cast<size_t>(NP) * u;
+  double x[NP], v[NP], pb[NP], pbf[NP];
+  ldv<NP>(S.pos + at, x);
+  ldv<NP>(S.vel + at, v);
+  ldv<NP>(S.pb + at, pb);
+  ldv<NP>(S.pbf + at, pbf);
+  Fit<F> acc[NP];
+  for (;;) {
+    uint32_t un = u, an = a + 1;
+    size_t atn = at + ld;
+    bool next = true;
+    if (an == d) {
+      an = 0;
+      un = u + stride;
+      atn = static_cast<size_t>(NP) * un;
+      next = un < u_end;
+    }
+    double xn[NP], vn[NP], pbn[NP], pbfn[NP];
+    if constexpr (CFG::kPF) {
+      if (next) {
+        ldv<NP>(S.pos + atn, xn);
+        ldv<NP>(S.vel + atn, vn);
+        ldv<NP>(S.pb + atn, pbn);
+        if (an == 0) ldv<NP>(S.pbf + atn, pbfn);
       }
+    }
+    const uint32_t li = NP * u;
+    const uint32_t g0 = P.base + li;
+    const double g = gpos[a];
+    double nx[NP], nv[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const double r1 = uniform01(P, t, g0 + k, a, 0);
+      const double r2 = uniform01(P, t, g0 + k, a, 1);
+      nv[k] = vel_step(P, v[k], x[k], pb[k], g, r1, r2);
+      nx[k] = pos_step(P, x[k], nv[k]);
+    }
+    stv<NP>(S.vel + at, nv);
+    stv<NP>(S.pos + at, nx);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) acc[k].add(nx[k], a);
+    if (a + 1 == d) {  // unit complete: pbest (swarm.hpp:100-108) + snapshot filter
+      bool upd[NP];
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const double f = acc[k].value();
+        acc[k] = Fit<F>();
+        const bool ok = k == 0 || li + k < P.n;
+        upd[k] = ok && f > pbf[k];
+        any |= upd[k];
+        if (upd[k]) S.pbf[li + k] = f;
+        if (ok && f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+          ++adm;
+          if (beats(f, g0 + k, bf, bi)) {
+            bf = f;
+            bi = g0 + k;
+          }
+        }
+      }
+      if (any) {  // rare after warm-up: re-read the just-written positions
+        for (uint32_t j = 0; j < d; ++j) {
+          const size_t aj = static_cast<size_t>(j) * ld + li;
+#pragma unroll
+          for (int k = 0; k < NP; ++k)
+            if (upd[k]) S.pb[aj + k] = S.pos[aj + k];
+        }
+      }
+    }
+    if (!next) break;
+    u = un;
+    a = an;
+    at = atn;
+    if constexpr (CFG::kPF) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        x[k] = xn[k];
+        v[k] = vn[k];
+        pb[k] = pbn[k];
+        if (an == 0) pbf[k] = pbfn[k];
+      }
+    } else {
+      ldv<NP>(S.pos + at, x);
+      ldv<NP>(S.vel + at, v);
+      ldv<NP>(S.pb + at, pb);
+      if (an == 0) ldv<NP>(S.pbf + at, pbf);
     }
   }
 }
 
-__device__ __forceinline__ void block_pair_range(const KParams& P, uint32_t& b, uint32_t& e) {
-  const uint64_t pairs = (P.n + 1ull) / 2;
-  b = static_cast<uint32_t>(pairs * blockIdx.x / gridDim.x);
-  e = static_cast<uint32_t>(pairs * (blockIdx.x + 1) / gridDim.x);
+template <int NP>
+__device__ __forceinline__ void block_unit_range(const KParams& P, uint32_t& b, uint32_t& e) {
+  const uint64_t units = (P.n + NP - 1ull) / NP;
+  b = static_cast<uint32_t>(units * blockIdx.x / gridDim.x);
+  e = static_cast<uint32_t>(units * (blockIdx.x + 1) / gridDim.x);
 }
 
 // --------------------------------------------------------- sync (fused)
-template <int F>
-__global__ void __launch_bounds__(kSyncThreads) k_sync(KParams P, KState S, KCtl C, uint32_t t0,
+template <int F, class CFG>
+__global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_sync(KParams P, KState S, KCtl C, uint32_t t0,
                                                        uint32_t t1) {
   extern __shared__ double s_gpos[];  // [d] iteration-start gbest position
   __shared__ BlockCand bc;
@@ -514,8 +717,6 @@ __global__ void __launch_bounds__(kSyncThreads) k_sync(KParams P, KState S, KCtl
   __syncthreads();
   double snap_fit = s_snap_fit;
   uint32_t snap_idx = s_snap_idx;
-  uint32_t p_begin, p_end;
-  block_pair_range(P, p_begin, p_end);
   const uint32_t cap = C.q_cap;
   uint32_t bar_target = 0;
 
@@ -523,7 +724,7 @@ __global__ void __launch_bounds__(kSyncThreads) k_sync(KParams P, KState S, KCtl
     const uint32_t qb = t % 3;
     double bf;
     uint32_t bi, adm;
-    step_pairs<F>(P, S, t, p_begin, p_end, s_gpos, snap_fit, bf, bi, adm);
+    step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
     warp_publish(bc, bf, bi, adm);
     __syncthreads();
 
@@ -628,8 +829,8 @@ __global__ void __launch_bounds__(kSyncThreads) k_sync(KParams P, KState S, KCtl
 // One iteration of the fused step on a shard; the last block to finish
 // reduces the grid queue to the shard's candidate record
 // {fit, particle, admitted, pos[d]} (sentinel when nothing was admitted).
-template <int F>
-__global__ void __launch_bounds__(kSyncThreads) k_propose(KParams P, KState S, KCtl C, uint32_t t,
+template <int F, class CFG>
+__global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_propose(KParams P, KState S, KCtl C, uint32_t t,
                                                           unsigned char* record) {
   extern __shared__ double s_gpos[];
   __shared__ BlockCand bc;
@@ -644,11 +845,9 @@ __global__ void __launch_bounds__(kSyncThreads) k_propose(KParams P, KState S, K
   }
   __syncthreads();
   const double snap_fit = C.snap->fit;
-  uint32_t p_begin, p_end;
-  block_pair_range(P, p_begin, p_end);
   double bf;
   uint32_t bi, adm;
-  step_pairs<F>(P, S, t, p_begin, p_end, s_gpos, snap_fit, bf, bi, adm);
+  step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
   warp_publish(bc, bf, bi, adm);
   __syncthreads();
   if (warp == 0) {
@@ -760,16 +959,14 @@ __global__ void k_commit(KParams P, KCtl C, uint32_t t, const unsigned char* rec
 // a seqlock: readers retry on an odd or changed version; a writer takes the
 // record with CAS(version: even -> odd), re-checks beats() under it, writes,
 // and releases with version+2. No grid barrier anywhere.
-template <int F>
-__global__ void __launch_bounds__(kSyncThreads) k_async(KParams P, KState S, KCtl C, uint32_t t0,
+template <int F, class CFG>
+__global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_async(KParams P, KState S, KCtl C, uint32_t t0,
                                                         uint32_t t1) {
   extern __shared__ double s_gpos[];
   __shared__ BlockCand bc;
   __shared__ double s_fit;
   __shared__ uint32_t s_idx, s_ver, s_have, s_ok;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t p_begin, p_end;
-  block_pair_range(P, p_begin, p_end);
   if (tid == 0) {
     s_have = 0;
     s_ver = 0xffffffffu;
@@ -813,7 +1010,7 @@ __global__ void __launch_bounds__(kSyncThreads) k_async(KParams P, KState S, KCt
     const double snap_fit = s_fit;
     double bf;
     uint32_t bi, adm;
-    step_pairs<F>(P, S, t, p_begin, p_end, s_gpos, snap_fit, bf, bi, adm);
+    step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
     warp_publish(bc, bf, bi, adm);
     __syncthreads();
     if (warp == 0) {
@@ -823,10 +1020,9 @@ __global__ void __launch_bounds__(kSyncThreads) k_async(KParams P, KState S, KCt
         double f = lane < nq ? bc.f[lane] : -INFINITY;
         uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
         warp_argmax(f, i);
-        // cheap pre-check against the live fit; re-checked under the CAS
-        const double lf0 = __ldcg(&C.live->fit);
-        const uint32_t lp0 = __ldcg(&C.live->particle);
-        if (beats(f, i, lf0, lp0)) {
+        // lock-free pre-check (may_beat); re-checked under the CAS
+        const double lf0 = ld_acquire_gpu_f64(&C.live->fit);
+        if (may_beat(C.live, f, i)) {
           uint32_t v = 0;
           if (lane == 0) {
             const uint64_t tl = globaltimer_ns();
@@ -844,10 +1040,8 @@ __global__ void __launch_bounds__(kSyncThreads) k_async(KParams P, KState S, KCt
           if (win) {
             for (uint32_t a = lane; a < P.d; a += 32)
               C.live_pos[a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
-            if (lane == 0) {
-              C.live->fit = f;
-              C.live->particle = i;
-            }
+            __syncwarp();
+            if (lane == 0) write_rec(C.live, f, i);
             view = f;
           } else {
             view = lf;

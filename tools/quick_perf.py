@@ -4,6 +4,7 @@ import numpy as np
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import paper_2205_01313_b200 as cp
 
+VARIANTS = [getattr(cp, v) for v in __import__("os").environ.get("QP_VARIANTS", "SYNC,ASYNC,QUEUE_LOCK,QUEUE,REDUCTION").split(",")]
 shapes = [("cubic", 1 << 20, 1, 200), ("cubic", 1 << 24, 1, 20), ("rastrigin", 1 << 20, 32, 10), ("sphere", 1 << 24, 8, 10)]
 if len(sys.argv) > 1:
     shapes = shapes[: int(sys.argv[1])]
@@ -11,7 +12,7 @@ for fit, n, d, T in shapes:
     f = cp.find_fitness(fit)
     p = cp.make_params(f, n, d, T)
     with cp.Swarm(p, f, 1) as sw:
-        for v in (cp.SYNC, cp.ASYNC, cp.QUEUE_LOCK, cp.QUEUE, cp.REDUCTION):
+        for v in VARIANTS:
             best = 1e9
             for rep in range(2):
                 sw.init()
