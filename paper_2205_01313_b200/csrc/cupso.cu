@@ -152,6 +152,7 @@ struct cupso_swarm {
   uint32_t groups = 0;
   int sync_grid = 0;
   int step_cfg = 0;
+  bool wave = false;
   uint32_t q_alloc = 0;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
   std::vector<uint8_t> is_async;
@@ -192,6 +193,7 @@ using Cfg3 = StepCfg<1, 1, 6>;
 using Cfg4 = StepCfg<2, 0, 6>;
 using Cfg5 = StepCfg<1, 0, 6>;
 constexpr int kNumCfg = 6;
+using WaveCfg = StepCfg<1, 0, 8>;  // one particle per thread, 32 registers, 64 warps/SM
 
 template <typename Fn>
 void dispatch_cfg(int c, Fn&& fn) {
@@ -203,6 +205,22 @@ void dispatch_cfg(int c, Fn&& fn) {
     case 4: fn(Cfg4{}); break;
     default: fn(Cfg5{}); break;
   }
+}
+
+// cuda-sync runs as one persistent cooperative kernel when the swarm is
+// L2-resident (latency/issue-bound: the grid barrier is cheaper than a launch)
+// and as a CUDA graph of one-wave-per-iteration launches when it streams
+// from HBM (occupancy-bound). Both are bit-identical; CUPSO_SYNC_MODE=
+// persistent|wave overrides.
+bool use_wave(const KParams& P) {
+  if (const char* e = getenv("CUPSO_SYNC_MODE")) {
+    if (!strcmp(e, "wave")) return true;
+    if (!strcmp(e, "persistent")) return false;
+  }
+  // measured on B200 (profiles/r01_sync_modes.txt): d=1 streams best as the
+  // persistent two-particles-per-thread kernel (LDG.128), d>=2 as waves
+  const double state_bytes = static_cast<double>(P.ld) * (3.0 * P.d + 1.0) * 8.0;
+  return P.d >= 2 && state_bytes > 64.0 * (1 << 20);
 }
 
 int default_step_cfg(const KParams& P) {
@@ -232,6 +250,8 @@ int num_sms(int device) {
 
 size_t sync_smem(const cupso_swarm* h) { return static_cast<size_t>(h->P.d) * sizeof(double); }
 constexpr uint32_t kMaxSyncDims = 12288;  // 96 KiB of dynamic smem for the gbest snapshot
+
+cupso_status ensure_queue(cupso_swarm* h, uint64_t cap);
 
 // Persistent grid: every block co-resident (required by the grid barrier).
 cupso_status ensure_sync_grid(cupso_swarm* h) {
@@ -267,17 +287,59 @@ cupso_status ensure_sync_grid(cupso_swarm* h) {
   const uint64_t min_work = std::max<uint64_t>(1, units / (2 * kSyncThreads));
   grid = std::max<uint64_t>(1, std::min(grid, min_work));
   h->sync_grid = static_cast<int>(grid);
-  if (h->q_alloc < grid) {
-    void *qf, *qi, *qp;
-    TRY(dmalloc(h, &qf, 3 * grid * sizeof(double)));
-    TRY(dmalloc(h, &qi, 3 * grid * sizeof(uint32_t)));
-    TRY(dmalloc(h, &qp, 3 * grid * h->P.d * sizeof(double)));
-    h->C.q_fit = static_cast<double*>(qf);
-    h->C.q_idx = static_cast<uint32_t*>(qi);
-    h->C.q_pos = static_cast<double*>(qp);
-    h->C.q_cap = static_cast<uint32_t>(grid);
-    h->q_alloc = static_cast<uint32_t>(grid);
+  TRY(ensure_queue(h, grid));
+  return CUPSO_OK;
+}
+
+cupso_status ensure_queue(cupso_swarm* h, uint64_t cap) {
+  if (h->q_alloc >= cap) return CUPSO_OK;
+  void *qf, *qi, *qp;
+  TRY(dmalloc(h, &qf, 3 * cap * sizeof(double)));
+  TRY(dmalloc(h, &qi, 3 * cap * sizeof(uint32_t)));
+  TRY(dmalloc(h, &qp, 3 * cap * h->P.d * sizeof(double)));
+  h->C.q_fit = static_cast<double*>(qf);
+  h->C.q_idx = static_cast<uint32_t*>(qi);
+  h->C.q_pos = static_cast<double*>(qp);
+  h->C.q_cap = static_cast<uint32_t>(cap);
+  h->q_alloc = static_cast<uint32_t>(cap);
+  h->graphs.clear();  // captured graphs hold the old queue pointers
+  return CUPSO_OK;
+}
+
+// Wave mode of cuda-sync: [t0, t0+iters) as one CUDA graph of k_wave launches.
+cupso_status wave_graph(cupso_swarm* h, uint32_t t0, uint32_t iters, cudaGraphExec_t* out) {
+  const uint32_t blocks = static_cast<uint32_t>((h->P.n + kSyncThreads - 1) / kSyncThreads);
+  TRY(ensure_queue(h, blocks));
+  const auto key = std::make_tuple(100 + CUPSO_SYNC, t0, iters);
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) {
+    *out = it->second;
+    return CUPSO_OK;
   }
+  if (h->P.d > kMaxSyncDims)
+    return fail(CUPSO_EINVAL, "cuda-sync: dims (%u) above %u", h->P.d, kMaxSyncDims);
+  const size_t smem = sync_smem(h);
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t le = cudaSuccess;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_wave<f, WaveCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (uint32_t t = t0; t < t0 + iters && le == cudaSuccess; ++t) {
+      k_wave<f, WaveCfg><<<blocks, kSyncThreads, smem, h->stream>>>(h->P, h->S, h->C, t);
+      le = cudaGetLastError();
+    }
+  });
+  cudaError_t ee = cudaStreamEndCapture(h->stream, &g);
+  CK(le);
+  CK(ee);
+  cudaGraphExec_t ge;
+  cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  CK(ie);
+  h->graphs[key] = ge;
+  *out = ge;
   return CUPSO_OK;
 }
 
@@ -414,12 +476,17 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   const uint32_t t0 = h->t, t1 = h->t + iters;
   cudaGraphExec_t ge = nullptr;
   if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
+  const bool wave = variant == CUPSO_SYNC && h->wave && !h->comm;
+  if (iters && wave) {
+    TRY(wave_graph(h, t0, iters, &ge));
+    CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
+  }
   if (iters && variant == CUPSO_QUEUE_LOCK) TRY(copy_record(h, h->C.live, h->C.snap));
   if (iters && variant == CUPSO_ASYNC) {
     TRY(copy_record(h, h->C.live, h->C.snap));
     CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
   }
-  if (iters && (variant == CUPSO_SYNC || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
+  if (iters && ((variant == CUPSO_SYNC && !wave) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
   CK(cudaEventRecord(h->ev0, h->stream));
   if (iters) {
     if (ge) {
@@ -486,6 +553,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   P.ld = (static_cast<uint64_t>(count) + 63) / 64 * 64;
   key_schedule(seed, P);
   h->step_cfg = default_step_cfg(P);
+  h->wave = use_wave(P);
   h->groups = (count + p->group_size - 1) / p->group_size;
   h->rec_bytes = sizeof(Rec) + sizeof(double) * p->dims;
   h->is_async.assign(h->T, 0);
@@ -508,7 +576,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   h->eval_buf = static_cast<double*>(ev);
   // control block: snap rec, live rec, 2 shard records, counters
   const size_t rb = (h->rec_bytes + 15) / 16 * 16;
-  const size_t ctl = 4 * rb + 64;
+  const size_t ctl = 4 * rb + 64 + 64 * sizeof(uint32_t);
   void *c, *tr, *ti, *adm, *tk, *af, *ai, *rall;
   if ((st = dmalloc(h, &c, ctl)) || (st = dmalloc(h, &tr, h->T * 8ull)) ||
       (st = dmalloc(h, &ti, h->T * 4ull)) || (st = dmalloc(h, &adm, h->T * 8ull)) ||
@@ -530,6 +598,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   C.bar = ctr + 2;
   C.seq = ctr + 3;
   C.q_count = ctr + 4;  // [3]
+  C.ticket_grp = ctr + 16;  // [64]
   C.trace = static_cast<double*>(tr);
   C.trace_idx = static_cast<uint32_t*>(ti);
   C.admitted = static_cast<unsigned long long*>(adm);

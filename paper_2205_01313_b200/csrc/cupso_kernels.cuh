@@ -47,6 +47,7 @@ struct KCtl {
   uint32_t* aux_idx;              // [groups]
   uint32_t* lock;                 // queue-lock spin lock word
   uint32_t* ticket;               // last-block-done counter
+  uint32_t* ticket_grp;           // [64] first-level counters of the hierarchical ticket
   uint32_t* bar;                  // grid barrier counter
   uint32_t* seq;                  // async seqlock version
   uint32_t* q_count;              // [3] grid queue fill counters
@@ -822,6 +823,140 @@ __global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_sync(KParams 
       *C.snap = r;
       *C.live = r;
     }
+  }
+}
+
+// Block-wide argmax over grid-queue entries [0, nq) of buffer qb (all threads
+// call; result broadcast through smem). Entries are deterministic, so every
+// block (or the single resolving block) picks the same winner.
+struct ResolveSmem {
+  double f[kSyncWarps];
+  uint32_t i[kSyncWarps], s[kSyncWarps];
+};
+__device__ __forceinline__ void resolve_queue(const KCtl& C, size_t base, uint32_t nq, ResolveSmem& rs,
+                                              double& wf, uint32_t& wi, uint32_t& ws) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double f = -INFINITY;
+  uint32_t i = kNoParticle, s = 0;
+  for (uint32_t k = tid; k < nq; k += blockDim.x) {
+    const double ef = __ldcg(&C.q_fit[base + k]);
+    const uint32_t ei = __ldcg(&C.q_idx[base + k]);
+    if (beats(ef, ei, f, i)) {
+      f = ef;
+      i = ei;
+      s = k;
+    }
+  }
+  warp_argmax3(f, i, s);
+  if (lane == 0) {
+    rs.f[warp] = f;
+    rs.i[warp] = i;
+    rs.s[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nw = blockDim.x >> 5;
+    f = lane < nw ? rs.f[lane] : -INFINITY;
+    i = lane < nw ? rs.i[lane] : kNoParticle;
+    s = lane < nw ? rs.s[lane] : 0;
+    warp_argmax3(f, i, s);
+    if (lane == 0) {
+      rs.f[0] = f;
+      rs.i[0] = i;
+      rs.s[0] = s;
+    }
+  }
+  __syncthreads();
+  wf = rs.f[0];
+  wi = rs.i[0];
+  ws = rs.s[0];
+}
+
+// Hierarchical "last block done": blocks first count on one of 64 counters
+// (blockIdx % 64) and only each group's last block touches the global
+// ticket, so a 131072-block launch puts ~2048 atomics on each of 64 L2
+// addresses instead of 131072 on one. Call from one thread after a fence.
+__device__ __forceinline__ bool last_block_done(const KCtl& C) {
+  const uint32_t G = gridDim.x;
+  const uint32_t grp = blockIdx.x & 63u;
+  const uint32_t ngrp = G < 64u ? G : 64u;
+  const uint32_t grp_size = (G - grp + 63u) / 64u;
+  if (atomicAdd(&C.ticket_grp[grp], 1u) != grp_size - 1u) return false;
+  C.ticket_grp[grp] = 0u;  // every block of the group has arrived
+  __threadfence();
+  if (atomicAdd(C.ticket, 1u) != ngrp - 1u) return false;
+  *C.ticket = 0u;
+  __threadfence();
+  return true;
+}
+
+// --------------------------------------------------------------- wave
+// One launch per iteration (captured in a CUDA graph): one unit per thread,
+// full occupancy, hardware block scheduling -- the HBM-bound shape of the
+// synchronous variant. Blocks append their winner to the grid queue (rare);
+// the last block resolves it into the snapshot record and trace[t]. No grid
+// barrier, no lock, and no atomics on the common path except the ticket.
+template <int F, class CFG>
+__global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_wave(KParams P, KState S, KCtl C,
+                                                                        uint32_t t) {
+  extern __shared__ double s_gpos[];
+  __shared__ BlockCand bc;
+  __shared__ ResolveSmem rs;
+  __shared__ int s_last;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  if (tid == 0) {
+    bc.n = 0;
+    bc.adm = 0;
+  }
+  __syncthreads();
+  const double snap_fit = C.snap->fit;
+  double bf;
+  uint32_t bi, adm;
+  step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
+  warp_publish(bc, bf, bi, adm);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nq = bc.n;
+    if (nq) {
+      double f = lane < nq ? bc.f[lane] : -INFINITY;
+      uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
+      warp_argmax(f, i);
+      uint32_t slot = 0;
+      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (lane == 0) {
+        C.q_fit[slot] = f;
+        C.q_idx[slot] = i;
+      }
+      for (uint32_t a = lane; a < P.d; a += 32)
+        C.q_pos[static_cast<size_t>(slot) * P.d + a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      if (bc.adm) atomicAdd(&C.admitted[t], bc.adm);
+      s_last = last_block_done(C);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const uint32_t nq = __ldcg(&C.q_count[0]);
+  if (nq) {
+    double wf;
+    uint32_t wi, ws;
+    resolve_queue(C, 0, nq, rs, wf, wi, ws);
+    for (uint32_t a = tid; a < P.d; a += blockDim.x)
+      C.snap_pos[a] = __ldcg(&C.q_pos[static_cast<size_t>(ws) * P.d + a]);
+    if (tid == 0) {  // every entry passed fit > snap_fit: adopt
+      C.snap->fit = wf;
+      C.snap->particle = wi;
+    }
+  }
+  if (tid == 0) {
+    C.trace[t] = nq ? rs.f[0] : snap_fit;
+    C.trace_idx[t] = nq ? rs.i[0] : C.snap->particle;
+    C.q_count[0] = 0;
   }
 }
 
