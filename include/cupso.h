@@ -160,6 +160,12 @@ int cupso_sync_grid_blocks(const cupso_swarm* h);    /* persistent grid size (af
  * cupso_shard_commit applies the same deterministic selection on every
  * shard (beats() among records, strict > against the snapshot). */
 size_t cupso_record_bytes(uint32_t dims);
+/* Initial exchange after cupso_init on every shard: export the shard's local
+ * initial gbest record, then adopt the beats()-max of all shards' records
+ * (the whole swarm's init_swarm argmax). NCCL-attached shards do this inside
+ * cupso_init. */
+cupso_status cupso_shard_snapshot(cupso_swarm* h, void* record_host);
+cupso_status cupso_shard_adopt(cupso_swarm* h, const void* records_host, uint32_t nrecords);
 cupso_status cupso_shard_propose(cupso_swarm* h, void* record_host);
 cupso_status cupso_shard_propose_device(cupso_swarm* h, void* record_dev);  /* stays on stream */
 cupso_status cupso_shard_commit(cupso_swarm* h, const void* records_host, uint32_t nrecords);

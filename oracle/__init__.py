@@ -109,6 +109,10 @@ class Oracle:
         L.orc_trimmed_mean.restype = C.c_double
         L.orc_trimmed_mean.argtypes = [C.POINTER(C.c_double), C.c_size_t]
         L.orc_trace_checksum.argtypes = [C.POINTER(C.c_double), C.c_size_t, C.c_char_p]
+        L.orc_shard_step.argtypes = [C.POINTER(orc_params), C.c_int, C.c_uint64, C.c_uint32, C.POINTER(orc_state),
+                                     C.c_uint32, C.c_uint32, C.POINTER(C.c_double), C.c_double,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_uint32)]
         L.orc_init_swarm.argtypes = [C.POINTER(orc_params), C.c_uint64, C.c_int, C.POINTER(orc_state),
                                      C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
 
@@ -164,6 +168,18 @@ class Oracle:
         self.L.orc_init_swarm(C.byref(p), seed, FITNESS.index(fitness), C.byref(s), C.byref(gf),
                               C.byref(gi), _dp(gp))
         return st, gf.value, gi.value, gp
+
+    def shard_step(self, fitness, params, seed, t, st, first, count, snap_pos, snap_fit):
+        """One iteration over [first, first+count) of the full state dict `st` (in place)."""
+        n, d = params.particle_cnt, params.dims
+        s = orc_state(n, d, _dp(st["positions"]), _dp(st["velocities"]), _dp(st["fitness"]),
+                      _dp(st["pbest_pos"]), _dp(st["pbest_fit"]))
+        bf, bi, adm = C.c_double(), C.c_uint32(), C.c_uint32()
+        bp = np.zeros(d)
+        sp = np.ascontiguousarray(snap_pos, dtype=np.float64)
+        self.L.orc_shard_step(C.byref(params), FITNESS.index(fitness), seed, t, C.byref(s), first, count,
+                              _dp(sp), snap_fit, C.byref(bf), C.byref(bi), _dp(bp), C.byref(adm))
+        return bf.value, bi.value, bp, adm.value
 
     def run_serial(self, fitness, particles, dims, iters, seed, params=None, want_state=True):
         p = params if params is not None else self.make_params(fitness, particles, dims, iters)

@@ -304,6 +304,34 @@ int orc_run_serial(const orc_params* p, int fid, uint64_t seed, orc_result* r,
   return 0;
 }
 
+/* TEST ONLY -- one iteration of the particles [first, first+count) of a
+ * full-size state, returning the shard's best candidate that passes the
+ * snapshot filter (engine_queue.hpp:44,91) in beats() order (engine.hpp:38-41).
+ * Lets the 2-rank gloo test replay the multi-GPU exchange protocol on CPU. */
+int orc_shard_step(const orc_params* p, int fid, uint64_t seed, uint32_t t, orc_state* s,
+                   uint32_t first, uint32_t count, const double* snap_pos, double snap_fit,
+                   double* best_fit, uint32_t* best_idx, double* best_pos, uint32_t* admitted) {
+  double bf = -INFINITY;
+  uint32_t bi = 0xffffffffu;
+  uint32_t adm = 0;
+  for (uint32_t i = first; i < first + count; ++i) {
+    const double fit = advance_particle(s, p, fid, seed, t, i, snap_pos);
+    if (fit > snap_fit) {
+      ++adm;
+      if (fit > bf || (fit == bf && i < bi)) {
+        bf = fit;
+        bi = i;
+      }
+    }
+  }
+  *best_fit = bf;
+  *best_idx = bi;
+  *admitted = adm;
+  for (uint32_t d = 0; d < s->dims; ++d)
+    best_pos[d] = bi == 0xffffffffu ? 0.0 : s->positions[soa(bi, d, s->particle_cnt)];
+  return 0;
+}
+
 /* bench.hpp:31-44 */
 void orc_trace_checksum(const double* trace, size_t n, char out[17]) {
   uint64_t h = 1469598103934665603ull;

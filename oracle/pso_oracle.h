@@ -86,6 +86,11 @@ void orc_init_swarm(const orc_params* p, uint64_t seed, int fid, orc_state* s,
 int orc_run_serial(const orc_params* p, int fid, uint64_t seed, orc_result* r,
                    orc_state* final_state, orc_observer obs, void* user);
 
+/* TEST ONLY: one iteration of particles [first, first+count), shard candidate out */
+int orc_shard_step(const orc_params* p, int fid, uint64_t seed, uint32_t t, orc_state* s,
+                   uint32_t first, uint32_t count, const double* snap_pos, double snap_fit,
+                   double* best_fit, uint32_t* best_idx, double* best_pos, uint32_t* admitted);
+
 /* bench.hpp:31-44 FNV-1a over trace bits; writes 16 hex digits + NUL */
 void orc_trace_checksum(const double* trace, size_t n, char out[17]);
 /* bench.hpp:20-28; returns NaN when n < 3 (reference throws) */

@@ -640,6 +640,15 @@ cupso_status init_impl(cupso_swarm* h) {
   CK(cudaMemsetAsync(h->C.trace_key, 0, h->T * 8ull, h->stream));
   CK(cudaMemsetAsync(h->C.trace, 0, h->T * 8ull, h->stream));
   CK(cudaMemsetAsync(h->C.trace_idx, 0xff, h->T * 4ull, h->stream));
+  if (h->comm) {  // sharded: the initial gbest is the argmax over all shards
+    CK(cudaMemcpyAsync(h->rec_local, h->C.snap, h->rec_bytes, cudaMemcpyDeviceToDevice, h->stream));
+    const int rc = nccl().allGather(h->rec_local, h->rec_all, h->rec_bytes, /*ncclInt8*/ 0, h->comm,
+                                    h->stream);
+    if (rc != 0) return fail(CUPSO_ERUNTIME, "ncclAllGather (init) failed (%d)", rc);
+    k_adopt<<<1, 256, 0, h->stream>>>(h->P, h->C, h->rec_all, static_cast<uint32_t>(h->nranks),
+                                      h->rec_bytes);
+    CK(cudaGetLastError());
+  }
   Rec r;
   CK(cudaMemcpyAsync(&r, h->C.snap, sizeof r, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -947,6 +956,35 @@ cupso_status cupso_shard_commit_device(cupso_swarm* h, const void* records_dev, 
   TRY(commit_launch(h, h->t, static_cast<const unsigned char*>(records_dev), nrecords));
   h->is_async[h->t] = 0;
   h->t += 1;
+  return CUPSO_OK;
+}
+
+cupso_status cupso_shard_snapshot(cupso_swarm* h, void* record_host) {
+  if (!h || !record_host) return fail(CUPSO_EINVAL, "null argument");
+  if (!h->initialized) return fail(CUPSO_ELOGIC, "snapshot before cupso_init");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(record_host, h->C.snap, h->rec_bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return CUPSO_OK;
+}
+
+cupso_status cupso_shard_adopt(cupso_swarm* h, const void* records_host, uint32_t nrecords) {
+  if (!h || !records_host) return fail(CUPSO_EINVAL, "null argument");
+  if (!h->initialized) return fail(CUPSO_ELOGIC, "adopt before cupso_init");
+  CK(cudaSetDevice(h->device));
+  void* d = nullptr;
+  CK(cudaMallocAsync(&d, h->rec_bytes * nrecords, h->stream));
+  CK(cudaMemcpyAsync(d, records_host, h->rec_bytes * nrecords, cudaMemcpyHostToDevice, h->stream));
+  k_adopt<<<1, 256, 0, h->stream>>>(h->P, h->C, static_cast<const unsigned char*>(d), nrecords, h->rec_bytes);
+  CK(cudaGetLastError());
+  cudaFreeAsync(d, h->stream);
+  Rec r;
+  CK(cudaMemcpyAsync(&r, h->C.snap, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->t == 0) {
+    h->initial_fit = r.fit;
+    h->initial_particle = r.particle;
+  }
   return CUPSO_OK;
 }
 

@@ -1089,6 +1089,38 @@ __global__ void k_commit(KParams P, KCtl C, uint32_t t, const unsigned char* rec
   }
 }
 
+// Initial gbest of a sharded swarm: every shard adopts the beats()-max of the
+// shards' local initial records (init_swarm's first strict max, swarm.hpp:164-170,
+// taken over the whole swarm).
+__global__ void k_adopt(KParams P, KCtl C, const unsigned char* records, uint32_t nrec,
+                        size_t rec_bytes) {
+  __shared__ int s_w;
+  if (threadIdx.x == 0) {
+    double bf = -INFINITY;
+    uint32_t bi = kNoParticle;
+    int w = -1;
+    for (uint32_t r = 0; r < nrec; ++r) {
+      const Rec* rec = reinterpret_cast<const Rec*>(records + r * rec_bytes);
+      if (rec->particle != kNoParticle && beats(rec->fit, rec->particle, bf, bi)) {
+        bf = rec->fit;
+        bi = rec->particle;
+        w = static_cast<int>(r);
+      }
+    }
+    s_w = w;
+    const Rec out{w >= 0 ? bf : -INFINITY, w >= 0 ? bi : kNoParticle, 0u};
+    *C.snap = out;
+    *C.live = out;
+  }
+  __syncthreads();
+  for (uint32_t a = threadIdx.x; a < P.d; a += blockDim.x) {
+    const double x = s_w >= 0
+        ? reinterpret_cast<const double*>(records + s_w * rec_bytes + sizeof(Rec))[a] : 0.0;
+    C.snap_pos[a] = x;
+    C.live_pos[a] = x;
+  }
+}
+
 // ---------------------------------------------------------------- async
 // Free-running blocks. The live record {fit, particle, pos[d]} is guarded by
 // a seqlock: readers retry on an odd or changed version; a writer takes the

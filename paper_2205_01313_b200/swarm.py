@@ -125,6 +125,16 @@ class Swarm:
     def record_bytes(self) -> int:
         return lib().cupso_record_bytes(self.params.dims)
 
+    def snapshot_record(self) -> bytes:
+        buf = C.create_string_buffer(self.record_bytes)
+        check(lib().cupso_shard_snapshot(self._h, buf))
+        return buf.raw
+
+    def adopt(self, records: list[bytes] | bytes) -> None:
+        blob = records if isinstance(records, (bytes, bytearray)) else b"".join(records)
+        buf = C.create_string_buffer(bytes(blob), len(blob))
+        check(lib().cupso_shard_adopt(self._h, buf, len(blob) // self.record_bytes))
+
     def propose(self) -> bytes:
         buf = C.create_string_buffer(self.record_bytes)
         check(lib().cupso_shard_propose(self._h, buf))
@@ -139,6 +149,24 @@ class Swarm:
     def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib().cupso_nccl_init(self._h, buf, nranks, rank))
+
+
+def init_shards(shards: list["Swarm"]) -> None:
+    """(Re)initialise host-exchanged shards: local init_swarm, then every shard
+    adopts the swarm-wide initial gbest."""
+    for sh in shards:
+        sh.init()
+    recs = [sh.snapshot_record() for sh in shards]
+    for sh in shards:
+        sh.adopt(recs)
+
+
+def step_shards(shards: list["Swarm"], iters: int = 1) -> None:
+    """cuda-sync over host-exchanged shards: propose, exchange, commit per iteration."""
+    for _ in range(iters):
+        recs = [sh.propose() for sh in shards]
+        for sh in shards:
+            sh.commit(recs)
 
 
 def decode_record(rec: bytes, dims: int):

@@ -1,0 +1,64 @@
+"""CPU: the bench protocol (bench.hpp) restated for the CUDA engines."""
+import io
+
+import numpy as np
+import pytest
+
+
+def test_trimmed_mean(cupso):
+    assert cupso.trimmed_mean([1.0, 2.0, 3.0]) == 2.0
+    xs = [0.5, 0.1, 0.9, 0.3, 0.7, 0.2, 0.8, 0.4, 0.6, 1.0]
+    s = sorted(xs)
+    assert cupso.trimmed_mean(xs) == sum(s[1:-1]) / 8
+    with pytest.raises(ValueError, match="at least 3 samples"):
+        cupso.trimmed_mean([1.0, 2.0])
+
+
+def test_checksum_matches_oracle_and_reference(cupso, oracle):
+    rng = np.random.default_rng(1)
+    for _ in range(5):
+        tr = rng.normal(size=200)
+        assert cupso.trace_checksum(tr) == oracle.checksum(tr)
+    assert cupso.trace_checksum([900000.0] * 1000) == "585d124f8e33b353"
+
+
+def test_checksum_matches_reference(cupso, reference):
+    tr = np.linspace(-3, 7, 77)
+    assert cupso.trace_checksum(tr) == reference.checksum(tr)
+
+
+def test_table_ratio_arithmetic(cupso):
+    # acceptance.cpp:233-251: 0.385 / 0.220 -> 1.75
+    def rec(engine, secs):
+        return cupso.bench_record(engine, 128, 1, 100000, 1, secs, 900000.0, "0")
+    md = cupso.render_table([rec("serial", [0.300, 0.385, 0.500]), rec("queue-lock", [0.100, 0.220, 0.900])])
+    assert "| 0.385 | 0.220 | 1.75 |" in md
+    with pytest.raises(ValueError, match="no serial baseline"):
+        cupso.render_table([rec("queue-lock", [0.1, 0.2, 0.3])])
+
+
+def test_csv_round_trip_is_lossless(cupso):
+    r = cupso.bench_record("cuda-sync", 64, 1, 50, 9, [0.1 + 1e-17 * k for k in range(10)],
+                           899999.99999999988, "0123456789abcdef")
+    buf = io.StringIO()
+    buf.write(cupso.csv_header + "\n")
+    for k in range(10):
+        cupso.write_csv_row(buf, r, k)
+    buf.seek(0)
+    back = cupso.read_csv(buf)
+    assert len(back) == 1
+    assert back[0].seconds == r.seconds
+    assert back[0].final_gbest_fit == r.final_gbest_fit
+    assert back[0].checksum == r.checksum
+    with pytest.raises(RuntimeError, match="bad CSV"):
+        cupso.read_csv(io.StringIO("nope\n"))
+
+
+def test_bench_config_validation(cupso):
+    with pytest.raises(ValueError, match="repeat must be >= 3"):
+        cupso.bench_config(repeat=2).validate()
+    with pytest.raises(ValueError, match="at least one seed"):
+        cupso.bench_config(seeds=[]).validate()
+    with pytest.raises(ValueError, match="unknown engine"):
+        cupso.bench_config(engine="serial").validate()
+    cupso.bench_config().validate()
