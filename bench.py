@@ -56,49 +56,64 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled every 5 ms through NVML
+    (the nvidia-smi query fields clocks.sm / clocks_event_reasons.*) during the
+    timed region; nvidia-smi itself is too slow for a ~100 ms region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,power.draw")
+    REASONS = {  # nvmlClocksEventReason* bit -> nvidia-smi field name
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown",
+    }
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.005):
         self.device = device
-        self.samples = []
+        self.period = period_s
+        self.sm, self.reasons, self.power = [], set(), []
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
+        self.error = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # reported, never fatal
+            self.error = str(e)
         return self
 
     def _run(self):
+        nv, h = self._nv, self._h
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+                self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+            except Exception as e:
+                self.error = str(e)
+                return
+            self._stop.wait(self.period)
 
     def __exit__(self, *exc):
         self._stop.set()
         if self._t:
-            self._t.join(timeout=6)
+            self._t.join(timeout=2)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [],
+                    "samples": 0, "error": self.error or "no samples"}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                "sm_min_mhz": min(self.sm), "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "power_w_max": max(self.power) if self.power else None, "source": "NVML, 5 ms"}
 
 
 def measured_peak_gbs():
@@ -221,7 +236,7 @@ def flush_l2(torch, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
@@ -301,10 +316,13 @@ def main():
 
     # ---- roofline of the dominant kernel (one launch = T iterations for the persistent kernels) ----
     bytes_per_pu = (5 * d + 1) * 8
-    launches_per_step = {"cuda-sync": 1 if world == 1 else 2 * T, "cuda-async": 1,
+    # cuda-sync runs persistent (1 cooperative launch per step; grid > 0) or as
+    # a graph of one wave per iteration (grid == 0); shards: propose+commit per iteration
+    persistent = variant_name == "cuda-async" or (variant_name == "cuda-sync" and world == 1 and grid > 0)
+    launches_per_step = {"cuda-sync": 1 if persistent else (2 * T if world > 1 else T), "cuda-async": 1,
                          "cuda-queue-lock": T, "cuda-queue": 2 * T, "cuda-reduction": 2 * T,
                          "cuda-unrolled": 2 * T}[variant_name]
-    iters_per_launch = T if variant_name in ("cuda-sync", "cuda-async") and world == 1 else 1
+    iters_per_launch = T if persistent else 1
     launch_secs = (dev_secs / K) / (T / iters_per_launch)
     alg_bytes = count * iters_per_launch * bytes_per_pu
     peak, peak_src = measured_peak_gbs()
@@ -314,7 +332,10 @@ def main():
         traffic = traffic * iters_per_launch / traffic_iters
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": f"k_sync<{fitness}>" if variant_name == "cuda-sync" else variant_name,
+                "kernel": {"cuda-sync": f"k_sync<{fitness}>" if persistent else f"k_wave<{fitness}>",
+                           "cuda-async": f"k_async<{fitness}>"}.get(variant_name, f"k_classic_step<{fitness}>"),
+                "traffic_note": "ncu dram read+write per launch (profiles/ncu_summary_r01.json); "
+                                "below alg bytes = L2-resident state, above = pbest write-backs",
                 "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
                 "bytes_per_particle_update": bytes_per_pu}
 

@@ -1,0 +1,88 @@
+"""Turn this round's ncu captures + launch list into the committed profiles/.
+
+    python tools/make_profiles.py r01
+writes profiles/<r>_ncu_summary.txt, profiles/ncu_summary_<r>.json (read by
+bench.py for roofline.traffic) and profiles/<r>_launches_cfg2.txt.
+"""
+import csv
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from ncu_summary import METRICS, raw, to_bytes  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+
+# capture -> (workload, variant, iterations per captured launch, particles scale to the workload)
+CAPTURES = {
+    "cfg2_sync": ("cfg2", "cuda-sync", 200, 1.0, "k_sync<cubic> persistent, 2^20 x d=1, one launch = 200 iterations"),
+    "cfg2_reduction_step": ("cfg2", "cuda-reduction", 1, 1.0, "k_classic_step<cubic,tree> (reduction phase 1), one iteration"),
+    "cfg2_reduction_fold": ("cfg2", "cuda-reduction-fold", 1, 1.0, "k_classic_fold<tree> (reduction phase 2), one iteration"),
+    "cfg3_async": ("cfg3", "cuda-async", 20, 1.0, "k_async<cubic>, 2^24 x d=1, one launch = 20 iterations"),
+    "cfg4_wave": ("cfg4", "cuda-sync", 1, 1.0, "k_wave<rastrigin>, 2^20 x d=32, one iteration (iteration 5)"),
+    "cfg5proxy_wave": ("cfg5", "cuda-sync", 1, 16.0, "k_wave<sphere>, 2^24 x d=8 proxy of 2^28 (x16 per launch), iteration 5"),
+}
+
+
+def main(tag):
+    lines = [f"# {tag}: ncu --set full --clock-control none captures (B200, sm_100a); one launch each",
+             "# per-launch numbers are cold-cache and serialised under replay; compare shares, not absolutes", ""]
+    js = {}
+    for key, (wl, var, iters, scale, desc) in CAPTURES.items():
+        rep = os.path.join(OUT, f"{tag}_{key}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        for d in raw(rep):
+            lines.append(f"== {key}: {desc}")
+            lines.append(f"   kernel: {d['kernel'][:110]}")
+            for m in METRICS:
+                if m in d:
+                    lines.append(f"   {m:62s} {d[m][0]} {d[m][1]}")
+            lines.append(f"   top stalls (warps per issue-active): {d['top_stalls']}")
+            rd = to_bytes(*d["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in d else None
+            wr = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
+            dur = d.get("gpu__time_duration.sum")
+            if rd is not None and wr is not None:
+                js.setdefault(wl, {})[var] = {
+                    "dram_bytes_per_launch": (rd + wr) * scale, "iters_per_launch": iters,
+                    "dram_read": rd * scale, "dram_write": wr * scale,
+                    "duration": dur, "capture": f"gpurun_out/{tag}_{key}.ncu-rep", "desc": desc}
+            lines.append("")
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    with open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.json"), "w") as fh:
+        json.dump(js, fh, indent=1)
+    # launch list of the default bench command
+    lp = os.path.join(OUT, "launches_cfg2.csv")
+    if os.path.exists(lp):
+        rows = list(csv.reader(open(lp)))
+        i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
+        hdr = rows[i]
+        ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+        agg = {}
+        for r in rows[i + 1:]:
+            if len(r) <= vi:
+                continue
+            try:
+                v = float(r[vi].replace(",", ""))
+            except ValueError:
+                continue
+            name = r[ki].split("(")[0]
+            a = agg.setdefault(name, [0, 0.0])
+            a[0] += 1
+            a[1] += v
+        tot = sum(a[1] for a in agg.values())
+        out = ["# launch list of `python bench.py --steps 3 --warmup 3 --no-cpu` under",
+               "# ncu --metrics gpu__time_duration.sum --clock-control none (serialised, cold: shares only)",
+               f"# {'launches':>8} {'total_us':>12} {'share':>6}  kernel"]
+        for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            out.append(f"  {c:8d} {t / 1e3:12.1f} {100 * t / tot:5.1f}%  {n}")
+        with open(os.path.join(ROOT, "profiles", f"{tag}_launches_cfg2.txt"), "w") as fh:
+            fh.write("\n".join(out) + "\n")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
