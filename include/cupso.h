@@ -149,6 +149,10 @@ cupso_status cupso_device_state(cupso_swarm* h, double** pos, double** vel, doub
                                 double** pbest_fit, uint64_t* ld);
 size_t cupso_device_bytes(const cupso_swarm* h);
 int cupso_sync_grid_blocks(const cupso_swarm* h);    /* persistent grid size (after a SYNC step) */
+/* How cuda-sync runs on this handle: 0 not yet decided, 1 persistent
+ * (k_sync), 2 graph of waves (k_wave), 3 SMEM-resident persistent
+ * (k_sync_res), 4 NCCL-sharded (k_propose/k_commit). */
+int cupso_sync_mode(const cupso_swarm* h);
 
 /* ---- multi-GPU shard exchange (one exchange step per iteration) ----
  * A candidate record is cupso_record_bytes(dims) bytes:

@@ -153,6 +153,10 @@ struct cupso_swarm {
   int sync_grid = 0;
   int step_cfg = 0;
   bool wave = false;
+  bool res_checked = false;    // SMEM-resident cuda-sync probed
+  int res_grid = 0;            // > 0: resident mode available (one block per SM)
+  uint32_t res_cap = 0;        // particles per block chunk (SMEM rows)
+  size_t res_smem = 0;
   uint32_t q_alloc = 0;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
   std::vector<uint8_t> is_async;
@@ -402,12 +406,74 @@ cupso_status classic_graph(cupso_swarm* h, int variant, uint32_t t0, uint32_t it
   return CUPSO_OK;
 }
 
+template <int F>
+const void* resident_kernel(uint32_t d) {
+  return d == 1 ? reinterpret_cast<const void*>(k_sync_res<F, 1>)
+                : reinterpret_cast<const void*>(k_sync_res<F, 0>);
+}
+
+// SMEM-resident mode of cuda-sync: one 1024-thread block per SM holding its
+// chunk of the swarm in shared memory for the whole launch. Possible when the
+// chunk's FP64 state (3d+1 doubles per particle) fits the opt-in SMEM limit.
+// Returns false (no error) when it does not fit; CUPSO_SYNC_MODE=persistent|wave
+// disables it.
+bool resident_fits(cupso_swarm* h) {
+  if (h->res_checked) return h->res_grid > 0;
+  h->res_checked = true;
+  if (const char* e = getenv("CUPSO_SYNC_MODE"))
+    if (strcmp(e, "resident") != 0 && strcmp(e, "auto") != 0) return false;
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
+    return false;
+  const int nsm = num_sms(h->device);
+  const uint64_t cap = (static_cast<uint64_t>(h->P.n) + nsm - 1) / nsm;
+  const uint64_t dpad = (h->P.d + 1ull) & ~1ull;
+  const uint64_t dyn = (dpad + (3ull * h->P.d + 1ull) * cap) * sizeof(double);
+  bool ok = false;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    const void* kfn = resident_kernel<f>(h->P.d);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kfn) != cudaSuccess) return;
+    if (dyn + fa.sharedSizeBytes > static_cast<uint64_t>(optin)) return;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)) !=
+        cudaSuccess)
+      return;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kResThreads, dyn) != cudaSuccess) return;
+    ok = per_sm >= 1;
+  });
+  cudaGetLastError();  // clear anything the probes left behind
+  if (!ok) return false;
+  if (ensure_queue(h, nsm) != CUPSO_OK) return false;
+  h->res_grid = nsm;
+  h->res_cap = static_cast<uint32_t>(cap);
+  h->res_smem = static_cast<size_t>(dyn);
+  return true;
+}
+
+cupso_status launch_resident(cupso_swarm* h, uint32_t t0, uint32_t t1) {
+  cudaError_t e = cudaSuccess;
+  CK(cudaMemsetAsync(h->C.bar, 0, sizeof(unsigned long long), h->stream));
+  CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    uint32_t cap = h->res_cap;
+    void* args[] = {&h->P, &h->S, &h->C, &t0, &t1, &cap};
+    e = cudaLaunchCooperativeKernel(resident_kernel<f>(h->P.d), dim3(h->res_grid), dim3(kResThreads), args,
+                                    h->res_smem, h->stream);
+  });
+  CK(e);
+  return CUPSO_OK;
+}
+
 cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_t t1) {
+  if (variant == CUPSO_SYNC && resident_fits(h)) return launch_resident(h, t0, t1);
   TRY(ensure_sync_grid(h));
   const size_t smem = sync_smem(h);
   cudaError_t e = cudaSuccess;
   // counters: bar (sync), seq (async), q_count[3]
-  CK(cudaMemsetAsync(h->C.bar, 0, sizeof(uint32_t), h->stream));
+  CK(cudaMemsetAsync(h->C.bar, 0, sizeof(unsigned long long), h->stream));
   CK(cudaMemsetAsync(h->C.seq, 0, sizeof(uint32_t), h->stream));
   CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
   dispatch_fit(h->fid, [&](auto F) {
@@ -486,6 +552,7 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
     TRY(copy_record(h, h->C.live, h->C.snap));
     CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
   }
+  if (iters && variant == CUPSO_SYNC && !wave && !h->comm) resident_fits(h);  // probe outside the timed region
   if (iters && ((variant == CUPSO_SYNC && !wave) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
   CK(cudaEventRecord(h->ev0, h->stream));
   if (iters) {
@@ -595,7 +662,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   uint32_t* ctr = reinterpret_cast<uint32_t*>(h->ctl_block + 4 * rb);
   C.lock = ctr + 0;
   C.ticket = ctr + 1;
-  C.bar = ctr + 2;
+  C.bar = reinterpret_cast<unsigned long long*>(ctr + 8);  // 8-byte aligned
   C.seq = ctr + 3;
   C.q_count = ctr + 4;  // [3]
   C.ticket_grp = ctr + 16;  // [64]
@@ -929,7 +996,18 @@ size_t cupso_device_bytes(const cupso_swarm* h) {
   return h->P.ld * (3ull * h->P.d + 2) * 8;
 }
 
-int cupso_sync_grid_blocks(const cupso_swarm* h) { return h ? h->sync_grid : 0; }
+int cupso_sync_grid_blocks(const cupso_swarm* h) {
+  if (!h) return 0;
+  return h->res_grid > 0 ? h->res_grid : h->sync_grid;
+}
+
+int cupso_sync_mode(const cupso_swarm* h) {
+  if (!h) return 0;
+  if (h->comm) return 4;
+  if (h->wave) return 2;
+  if (h->res_grid > 0) return 3;
+  return h->sync_grid > 0 ? 1 : 0;
+}
 
 size_t cupso_record_bytes(uint32_t dims) { return sizeof(Rec) + sizeof(double) * dims; }
 

@@ -48,7 +48,7 @@ struct KCtl {
   uint32_t* lock;                 // queue-lock spin lock word
   uint32_t* ticket;               // last-block-done counter
   uint32_t* ticket_grp;           // [64] first-level counters of the hierarchical ticket
-  uint32_t* bar;                  // grid barrier counter
+  unsigned long long* bar;        // grid barrier word (arrivals | appends << 32)
   uint32_t* seq;                  // async seqlock version
   uint32_t* q_count;              // [3] grid queue fill counters
   double* q_fit;                  // [3*cap]
@@ -476,10 +476,10 @@ __global__ void k_classic_fold(KParams P, KState S, KCtl C, uint32_t t, uint32_t
 // ---------------------------------------------------- shared block logic
 // Per-thread candidate over the thread's pairs -> block queue in smem via
 // warp ballot + shuffle argmax (one append per warp with a candidate).
+constexpr int kMaxWarps = 32;
 struct BlockCand {
-  double f[kSyncWarps];
-  uint32_t i[kSyncWarps];
-  uint32_t s[kSyncWarps];
+  double f[kMaxWarps];
+  uint32_t i[kMaxWarps];
   uint32_t n;
   unsigned long long adm;
 };
@@ -697,141 +697,12 @@ __device__ __forceinline__ void block_unit_range(const KParams& P, uint32_t& b, 
   e = static_cast<uint32_t>(units * (blockIdx.x + 1) / gridDim.x);
 }
 
-// --------------------------------------------------------- sync (fused)
-template <int F, class CFG>
-__global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_sync(KParams P, KState S, KCtl C, uint32_t t0,
-                                                       uint32_t t1) {
-  extern __shared__ double s_gpos[];  // [d] iteration-start gbest position
-  __shared__ BlockCand bc;
-  __shared__ double s_rf[kSyncWarps];
-  __shared__ uint32_t s_ri[kSyncWarps], s_rs[kSyncWarps];
-  __shared__ double s_snap_fit;
-  __shared__ uint32_t s_snap_idx, s_win_slot;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
-  if (tid == 0) {
-    s_snap_fit = C.snap->fit;
-    s_snap_idx = C.snap->particle;
-    bc.n = 0;
-    bc.adm = 0;
-  }
-  __syncthreads();
-  double snap_fit = s_snap_fit;
-  uint32_t snap_idx = s_snap_idx;
-  const uint32_t cap = C.q_cap;
-  uint32_t bar_target = 0;
-
-  for (uint32_t t = t0; t < t1; ++t) {
-    const uint32_t qb = t % 3;
-    double bf;
-    uint32_t bi, adm;
-    step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
-    warp_publish(bc, bf, bi, adm);
-    __syncthreads();
-
-    if (warp == 0) {  // block winner -> grid queue; then the grid barrier
-      const uint32_t nq = bc.n;
-      if (nq) {
-        double f = lane < nq ? bc.f[lane] : -INFINITY;
-        uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
-        warp_argmax(f, i);
-        uint32_t slot = 0;
-        if (lane == 0) slot = atomicAdd(&C.q_count[qb], 1u);
-        slot = __shfl_sync(0xffffffffu, slot, 0);
-        const size_t e = static_cast<size_t>(qb) * cap + slot;
-        if (lane == 0) {
-          C.q_fit[e] = f;
-          C.q_idx[e] = i;
-        }
-        for (uint32_t a = lane; a < P.d; a += 32)
-          C.q_pos[e * P.d + a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
-      }
-      if (lane == 0) {
-        if (bc.adm) atomicAdd(&C.admitted[t], bc.adm);
-        if (blockIdx.x == 0) C.q_count[(t + 1) % 3] = 0;  // last read two barriers ago
-      }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) {
-        bar_target += gridDim.x;
-        red_release_gpu_add(C.bar, 1u);
-        const uint64_t ts = globaltimer_ns();
-        while (ld_acquire_gpu(C.bar) < bar_target) {
-          if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
-        }
-        __threadfence();
-      }
-    }
-    __syncthreads();
-
-    // resolve: every block reduces the grid queue itself (deterministic)
-    const uint32_t nq = __ldcg(&C.q_count[qb]);
-    if (nq) {
-      double f = -INFINITY;
-      uint32_t i = kNoParticle, s = 0;
-      for (uint32_t k = tid; k < nq; k += blockDim.x) {
-        const size_t e = static_cast<size_t>(qb) * cap + k;
-        const double ef = __ldcg(&C.q_fit[e]);
-        const uint32_t ei = __ldcg(&C.q_idx[e]);
-        if (beats(ef, ei, f, i)) {
-          f = ef;
-          i = ei;
-          s = k;
-        }
-      }
-      warp_argmax3(f, i, s);
-      if (lane == 0) {
-        s_rf[warp] = f;
-        s_ri[warp] = i;
-        s_rs[warp] = s;
-      }
-      __syncthreads();
-      if (warp == 0) {
-        f = lane < kSyncWarps ? s_rf[lane] : -INFINITY;
-        i = lane < kSyncWarps ? s_ri[lane] : kNoParticle;
-        s = lane < kSyncWarps ? s_rs[lane] : 0;
-        warp_argmax3(f, i, s);
-        if (lane == 0) {  // every entry passed fit > snap_fit, so the winner is adopted
-          s_snap_fit = f;
-          s_snap_idx = i;
-          s_win_slot = s;
-        }
-      }
-      __syncthreads();
-      snap_fit = s_snap_fit;
-      snap_idx = s_snap_idx;
-      const size_t e = static_cast<size_t>(qb) * cap + s_win_slot;
-      for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.q_pos[e * P.d + a]);
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-      C.trace[t] = snap_fit;
-      C.trace_idx[t] = snap_idx;
-    }
-    if (tid == 0) {
-      bc.n = 0;
-      bc.adm = 0;
-    }
-    __syncthreads();
-  }
-  if (blockIdx.x == 0) {
-    for (uint32_t a = tid; a < P.d; a += blockDim.x) {
-      C.snap_pos[a] = s_gpos[a];
-      C.live_pos[a] = s_gpos[a];
-    }
-    if (tid == 0) {
-      const Rec r{snap_fit, snap_idx, 0u};
-      *C.snap = r;
-      *C.live = r;
-    }
-  }
-}
-
 // Block-wide argmax over grid-queue entries [0, nq) of buffer qb (all threads
 // call; result broadcast through smem). Entries are deterministic, so every
 // block (or the single resolving block) picks the same winner.
 struct ResolveSmem {
-  double f[kSyncWarps];
-  uint32_t i[kSyncWarps], s[kSyncWarps];
+  double f[kMaxWarps];
+  uint32_t i[kMaxWarps], s[kMaxWarps];
 };
 __device__ __forceinline__ void resolve_queue(const KCtl& C, size_t base, uint32_t nq, ResolveSmem& rs,
                                               double& wf, uint32_t& wi, uint32_t& ws) {
@@ -870,6 +741,241 @@ __device__ __forceinline__ void resolve_queue(const KCtl& C, size_t base, uint32
   wf = rs.f[0];
   wi = rs.i[0];
   ws = rs.s[0];
+}
+
+// Shared tail of the persistent synchronous kernels, called by all threads
+// once the block's candidates are in sh.bc (after a __syncthreads): warp 0
+// appends the block winner {fit, idx, pos[d]} to the grid queue (pos_of(a, i)
+// reads the winner's freshly written axis a), arrives at / waits on the grid
+// barrier, then every block resolves the (usually empty) queue itself into the
+// iteration-end snapshot. Deterministic whatever the arrival order.
+struct SyncShared {
+  BlockCand bc;
+  ResolveSmem rs;
+  uint32_t need;  // grid queue of this iteration may be non-empty
+};
+
+// Grid barrier word: low 32 bits count arrivals, high 32 bits count blocks
+// that appended a candidate. A spinner that sees the high half unchanged
+// knows the iteration admitted nothing (the common case after warm-up) and
+// skips the queue entirely -- no extra L2 round trip on the critical path.
+struct BarState {
+  uint32_t target = 0;   // arrivals expected so far in this launch
+  uint32_t appends = 0;  // exact appends counted through the end of the last iteration
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <class PosFn>
+__device__ __forceinline__ void sync_tail(const KParams& P, const KCtl& C, uint32_t t, SyncShared& sh,
+                                          double* s_gpos, double& snap_fit, uint32_t& snap_idx,
+                                          BarState& bs, PosFn pos_of) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cap = C.q_cap, qb = t % 3;
+  if (warp == 0) {  // block winner -> grid queue; then the grid barrier
+    const uint32_t nq = sh.bc.n;
+    if (nq) {
+      double f = lane < nq ? sh.bc.f[lane] : -INFINITY;
+      uint32_t i = lane < nq ? sh.bc.i[lane] : kNoParticle;
+      warp_argmax(f, i);
+      uint32_t slot = 0;
+      if (lane == 0) slot = atomicAdd(&C.q_count[qb], 1u);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      const size_t e = static_cast<size_t>(qb) * cap + slot;
+      if (lane == 0) {
+        C.q_fit[e] = f;
+        C.q_idx[e] = i;
+      }
+      for (uint32_t a = lane; a < P.d; a += 32) C.q_pos[e * P.d + a] = pos_of(a, i);
+      __threadfence();  // entry visible before the release below
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (sh.bc.adm) atomicAdd(&C.admitted[t], sh.bc.adm);
+      sh.bc.n = 0;  // the other warps are parked at the __syncthreads below
+      sh.bc.adm = 0;
+      if (blockIdx.x == 0) C.q_count[(t + 1) % 3] = 0;  // last read two barriers ago
+      bs.target += gridDim.x;
+      red_release_gpu_add_u64(C.bar, 1ull | (nq ? (1ull << 32) : 0ull));
+      const uint64_t ts = globaltimer_ns();
+      unsigned long long v;
+      while (static_cast<uint32_t>(v = ld_acquire_gpu_u64(C.bar)) < bs.target) {
+        if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+      }
+      // a faster block may already have arrived at the next barrier; any
+      // change of the high half only means "look at the queue"
+      sh.need = static_cast<uint32_t>(v >> 32) != bs.appends;
+    }
+  }
+  __syncthreads();
+  if (sh.need) {  // block-uniform
+    __threadfence();
+    const uint32_t nq = __ldcg(&C.q_count[qb]);
+    if (tid == 0) bs.appends += nq;  // exact appends of iteration t
+    if (nq) {
+      double wf;
+      uint32_t wi, ws;
+      resolve_queue(C, static_cast<size_t>(qb) * cap, nq, sh.rs, wf, wi, ws);
+      snap_fit = wf;  // every entry passed fit > snap_fit, so the winner is adopted
+      snap_idx = wi;
+      const size_t e = static_cast<size_t>(qb) * cap + ws;
+      for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.q_pos[e * P.d + a]);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    C.trace[t] = snap_fit;
+    C.trace_idx[t] = snap_idx;
+  }
+}
+
+__device__ __forceinline__ void write_final_record(const KParams& P, const KCtl& C, const double* s_gpos,
+                                                   double snap_fit, uint32_t snap_idx) {
+  if (blockIdx.x != 0) return;
+  for (uint32_t a = threadIdx.x; a < P.d; a += blockDim.x) {
+    C.snap_pos[a] = s_gpos[a];
+    C.live_pos[a] = s_gpos[a];
+  }
+  if (threadIdx.x == 0) {
+    const Rec r{snap_fit, snap_idx, 0u};
+    *C.snap = r;
+    *C.live = r;
+  }
+}
+
+// --------------------------------------------------------- sync (fused)
+template <int F, class CFG>
+__global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_sync(KParams P, KState S, KCtl C, uint32_t t0,
+                                                       uint32_t t1) {
+  extern __shared__ double s_gpos[];  // [d] iteration-start gbest position
+  __shared__ SyncShared sh;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  if (tid == 0) {
+    sh.bc.n = 0;
+    sh.bc.adm = 0;
+  }
+  double snap_fit = C.snap->fit;
+  uint32_t snap_idx = C.snap->particle;
+  __syncthreads();
+  BarState bs;
+  auto pos_of = [&](uint32_t a, uint32_t i) { return S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)]; };
+  for (uint32_t t = t0; t < t1; ++t) {
+    double bf;
+    uint32_t bi, adm;
+    step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
+    warp_publish(sh.bc, bf, bi, adm);
+    __syncthreads();
+    sync_tail(P, C, t, sh, s_gpos, snap_fit, snap_idx, bs, pos_of);
+  }
+  write_final_record(P, C, s_gpos, snap_fit, snap_idx);
+}
+
+// ------------------------------------------------ sync, SMEM-resident
+// The whole swarm lives in shared memory for the duration of the launch
+// when its FP64 state fits: one 1024-thread block per SM owns a contiguous
+// chunk of particles, stored axis-major in SMEM as x|v|pbest|pbest_fit.
+// Per iteration there is no global-memory traffic for the state at all --
+// only Philox/FP64 issue plus the grid barrier (cfg2: 2^20 x d=1 = 32 MB
+// over 148 x 227 KB). State is loaded at launch start and written back at
+// the end, so every launch boundary leaves HBM exact.
+constexpr int kResThreads = 1024;
+
+// D > 0 fixes the dimension at compile time (D = 1 is the BASELINE cfg2/cfg3
+// shape): the axis counter then constant-folds into the first Philox rounds
+// and the per-axis index arithmetic disappears.
+template <int F, int D = 0>
+__global__ void __launch_bounds__(kResThreads, 1) k_sync_res(KParams P, KState S, KCtl C, uint32_t t0,
+                                                              uint32_t t1, uint32_t chunk_cap) {
+  extern __shared__ double smem[];
+  __shared__ SyncShared sh;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t d = D > 0 ? static_cast<uint32_t>(D) : P.d;
+  const uint32_t c0 = static_cast<uint32_t>(static_cast<uint64_t>(P.n) * blockIdx.x / gridDim.x);
+  const uint32_t c1 = static_cast<uint32_t>(static_cast<uint64_t>(P.n) * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t m = c1 - c0;
+  const uint32_t dpad = (d + 1u) & ~1u;
+  double* s_gpos = smem;
+  double* sx = smem + dpad;
+  double* sv = sx + static_cast<size_t>(d) * chunk_cap;
+  double* spb = sv + static_cast<size_t>(d) * chunk_cap;
+  double* spbf = spb + static_cast<size_t>(d) * chunk_cap;
+  for (uint32_t a = 0; a < d; ++a) {
+    const size_t g = static_cast<size_t>(a) * P.ld + c0;
+    const size_t l = static_cast<size_t>(a) * chunk_cap;
+    for (uint32_t j = tid; j < m; j += blockDim.x) {
+      sx[l + j] = S.pos[g + j];
+      sv[l + j] = S.vel[g + j];
+      spb[l + j] = S.pb[g + j];
+    }
+  }
+  for (uint32_t j = tid; j < m; j += blockDim.x) spbf[j] = S.pbf[c0 + j];
+  for (uint32_t a = tid; a < d; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  if (tid == 0) {
+    sh.bc.n = 0;
+    sh.bc.adm = 0;
+  }
+  double snap_fit = C.snap->fit;
+  uint32_t snap_idx = C.snap->particle;
+  __syncthreads();
+  BarState bs;
+  const uint32_t gbase = P.base + c0;
+  auto pos_of = [&](uint32_t a, uint32_t i) { return sx[static_cast<size_t>(a) * chunk_cap + (i - gbase)]; };
+  for (uint32_t t = t0; t < t1; ++t) {
+    double bf = -INFINITY;
+    uint32_t bi = kNoParticle, adm = 0;
+    for (uint32_t j = tid; j < m; j += blockDim.x) {
+      const uint32_t gi = gbase + j;
+      Fit<F> acc;
+      for (uint32_t a = 0; a < d; ++a) {
+        const size_t l = static_cast<size_t>(a) * chunk_cap + j;
+        const double r1 = uniform01(P, t, gi, a, 0);
+        const double r2 = uniform01(P, t, gi, a, 1);
+        const double x = sx[l];
+        const double nv = vel_step(P, sv[l], x, spb[l], s_gpos[a], r1, r2);
+        const double nx = pos_step(P, x, nv);
+        sv[l] = nv;
+        sx[l] = nx;
+        acc.add(nx, a);
+      }
+      const double f = acc.value();
+      if (f > spbf[j]) {  // update_pbest (swarm.hpp:100-108)
+        spbf[j] = f;
+        for (uint32_t a = 0; a < d; ++a) {
+          const size_t l = static_cast<size_t>(a) * chunk_cap + j;
+          spb[l] = sx[l];
+        }
+      }
+      if (f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+        ++adm;
+        if (beats(f, gi, bf, bi)) {
+          bf = f;
+          bi = gi;
+        }
+      }
+    }
+    warp_publish(sh.bc, bf, bi, adm);
+    __syncthreads();
+    sync_tail(P, C, t, sh, s_gpos, snap_fit, snap_idx, bs, pos_of);
+  }
+  for (uint32_t a = 0; a < d; ++a) {
+    const size_t g = static_cast<size_t>(a) * P.ld + c0;
+    const size_t l = static_cast<size_t>(a) * chunk_cap;
+    for (uint32_t j = tid; j < m; j += blockDim.x) {
+      S.pos[g + j] = sx[l + j];
+      S.vel[g + j] = sv[l + j];
+      S.pb[g + j] = spb[l + j];
+    }
+  }
+  for (uint32_t j = tid; j < m; j += blockDim.x) S.pbf[c0 + j] = spbf[j];
+  write_final_record(P, C, s_gpos, snap_fit, snap_idx);
 }
 
 // Hierarchical "last block done": blocks first count on one of 64 counters

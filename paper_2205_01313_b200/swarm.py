@@ -117,6 +117,11 @@ class Swarm:
     def sync_grid_blocks(self) -> int:
         return lib().cupso_sync_grid_blocks(self._h)
 
+    SYNC_MODES = {0: "undecided", 1: "persistent", 2: "wave", 3: "resident", 4: "nccl-sharded"}
+
+    def sync_mode(self) -> str:
+        return self.SYNC_MODES[lib().cupso_sync_mode(self._h)]
+
     def stream(self) -> int:
         return lib().cupso_stream(self._h) or 0
 
