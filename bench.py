@@ -125,20 +125,25 @@ def measured_peak_gbs():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(workload: str, variant: str):
-    """dram bytes per launch from the committed ncu summary, or None."""
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
-            os.path.join(ROOT, "profiles")) else []:
+def ncu_entry(workload: str, variant: str) -> dict:
+    """The committed ncu summary entry (profiles/ncu_summary_*.json) for a kernel, or {}."""
+    pdir = os.path.join(ROOT, "profiles")
+    for name in sorted(os.listdir(pdir), reverse=True) if os.path.isdir(pdir) else []:
         if name.startswith("ncu_summary") and name.endswith(".json"):
             try:
-                with open(os.path.join(ROOT, "profiles", name)) as fh:
-                    d = json.load(fh)
-                e = d.get(workload, {}).get(variant)
+                with open(os.path.join(pdir, name)) as fh:
+                    e = json.load(fh).get(workload, {}).get(variant)
                 if e and e.get("dram_bytes_per_launch") is not None:
-                    return e["dram_bytes_per_launch"], e.get("iters_per_launch")
+                    return e
             except Exception:
                 pass
-    return None, None
+    return {}
+
+
+def ncu_traffic(workload: str, variant: str):
+    """dram bytes per launch from the committed ncu summary, or None."""
+    e = ncu_entry(workload, variant)
+    return (e["dram_bytes_per_launch"], e.get("iters_per_launch")) if e else (None, None)
 
 
 def cpu_reference_leg(fitness, n, d, max_seconds=12.0, sample_iters=None):
@@ -330,14 +335,36 @@ def main():
     traffic, traffic_iters = ncu_traffic(args.workload, variant_name)
     if traffic is not None and traffic_iters:
         traffic = traffic * iters_per_launch / traffic_iters
+    mode = sw.sync_mode() if variant_name == "cuda-sync" else None
+    sync_kernel = {"resident": f"k_sync_res<{fitness},{d if d == 1 else 0}>", "persistent": f"k_sync<{fitness}>",
+                   "wave": f"k_wave<{fitness}>"}.get(mode, f"k_propose<{fitness}>+k_commit")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": {"cuda-sync": f"k_sync<{fitness}>" if persistent else f"k_wave<{fitness}>",
+                "kernel": {"cuda-sync": sync_kernel,
                            "cuda-async": f"k_async<{fitness}>"}.get(variant_name, f"k_classic_step<{fitness}>"),
                 "traffic_note": "ncu dram read+write per launch (profiles/ncu_summary_r01.json); "
                                 "below alg bytes = L2-resident state, above = pbest write-backs",
                 "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
                 "bytes_per_particle_update": bytes_per_pu}
+    if mode == "resident":
+        # The swarm lives in SMEM for the whole launch: HBM carries ~0 bytes per
+        # iteration, so the algorithmic-bytes figure above can exceed
+        # the HBM roof. The binding roof is instruction issue (Philox IMAD/LOP3 +
+        # FP64): executed warp-instructions per iteration from the committed ncu
+        # capture vs 148 SMs x 4 schedulers x SM clock.
+        e = ncu_entry(args.workload, variant_name)
+        if e.get("warp_inst_per_launch"):
+            winst_iter = e["warp_inst_per_launch"] / e["iters_per_launch"]
+            sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            ach = winst_iter * T * K / dev_secs
+            roofline["issue_roofline"] = {
+                "bound": "issue", "achieved": ach / 1e9, "peak": nsm * 4 * sm_hz / 1e9,
+                "unit": "G warp-instructions/s", "frac": ach / (nsm * 4 * sm_hz),
+                "inst_per_particle_update": winst_iter * 32 / count,
+                "source": "smsp__inst_executed.sum of " + e.get("capture", "?")}
+        roofline["note"] = ("SMEM-resident swarm (k_sync_res): state read/written once per launch, not per "
+                            "iteration; frac > 1 means the HBM model does not bind -- see issue_roofline")
 
     extra = {}
     # ---- the in-repo reduction baseline kernel on the same workload (rank 0, N=1) ----

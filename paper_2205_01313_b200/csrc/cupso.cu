@@ -1109,17 +1109,63 @@ cupso_status cupso_nccl_init(cupso_swarm* h, const void* unique_id, int nranks, 
 
 void* cupso_stream(cupso_swarm* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
+}  // extern "C"
+
 // ------------------------------------------------------------- one-shot run
+namespace {
+// One cached swarm per thread (handles are not thread-safe; separate threads
+// keep separate swarms). Deliberately never destroyed at exit: freeing CUDA
+// memory during static destruction is unsafe, and the process is ending.
+struct RunCache {
+  cupso_swarm* h = nullptr;
+  cupso_params p{};
+  int fid = -1, device = -1;
+  cupso_swarm* take(const cupso_params* q, int f, int dev) {
+    if (h && fid == f && device == dev && std::memcmp(&p, q, sizeof p) == 0) {
+      cupso_swarm* r = h;
+      h = nullptr;
+      return r;
+    }
+    return nullptr;
+  }
+  void put(cupso_swarm* s) {
+    if (h && h != s) cupso_destroy(h);
+    h = s;
+    p = s->gp;
+    fid = s->fid;
+    device = s->device;
+  }
+};
+RunCache& run_cache() {
+  static thread_local RunCache* c = new RunCache();
+  return *c;
+}
+}  // namespace
+
+extern "C" {
 cupso_status cupso_run(const cupso_params* p, int fid, uint64_t seed, int variant, int device,
                        cupso_observer_fn observer, void* user, cupso_result* out) {
   if (!out) return fail(CUPSO_EINVAL, "null result");
   TRY(validate(p));
   if (variant < 0 || variant >= kNumVar) return fail(CUPSO_EINVAL, "unknown variant %d", variant);
-  cupso_swarm* h = nullptr;
-  TRY(cupso_create(p, fid, seed, device, &h));
+  // Repeated runs of the same shape on a thread reuse the device swarm
+  // (allocation, stream, events, probes) instead of re-creating it; only the
+  // Philox key schedule changes with the seed. Graphs bake kernel parameters
+  // in at capture, so they are dropped when the seed changes.
+  cupso_swarm* h = run_cache().take(p, fid, device);
+  if (h) {
+    if (h->seed != seed) {
+      for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+      h->graphs.clear();
+      h->seed = seed;
+      key_schedule(seed, h->P);
+    }
+  } else {
+    TRY(cupso_create(p, fid, seed, device, &h));
+  }
   struct Guard {
     cupso_swarm* h;
-    ~Guard() { cupso_destroy(h); }
+    ~Guard() { run_cache().put(h); }
   } guard{h};
   TRY(init_impl(h));
   out->initial_gbest_fit = h->initial_fit;

@@ -773,6 +773,80 @@ __device__ __forceinline__ void red_release_gpu_add_u64(unsigned long long* p, u
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// First half of sync_tail: warp 0 publishes the block winner and arrives at
+// the grid barrier (release). The caller may do gbest-independent work (the
+// next iteration's Philox draws) before sync_wait() blocks on the barrier.
+template <class PosFn>
+__device__ __forceinline__ void sync_arrive(const KParams& P, const KCtl& C, uint32_t t, SyncShared& sh,
+                                            BarState& bs, uint32_t& nq_out, PosFn pos_of) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cap = C.q_cap, qb = t % 3;
+  if (warp != 0) return;
+  const uint32_t nq = sh.bc.n;
+  nq_out = nq;
+  if (nq) {
+    double f = lane < nq ? sh.bc.f[lane] : -INFINITY;
+    uint32_t i = lane < nq ? sh.bc.i[lane] : kNoParticle;
+    warp_argmax(f, i);
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(&C.q_count[qb], 1u);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    const size_t e = static_cast<size_t>(qb) * cap + slot;
+    if (lane == 0) {
+      C.q_fit[e] = f;
+      C.q_idx[e] = i;
+    }
+    for (uint32_t a = lane; a < P.d; a += 32) C.q_pos[e * P.d + a] = pos_of(a, i);
+    __threadfence();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (sh.bc.adm) atomicAdd(&C.admitted[t], sh.bc.adm);
+    sh.bc.n = 0;
+    sh.bc.adm = 0;
+    if (blockIdx.x == 0) C.q_count[(t + 1) % 3] = 0;
+    bs.target += gridDim.x;
+    red_release_gpu_add_u64(C.bar, 1ull | (nq ? (1ull << 32) : 0ull));
+  }
+}
+
+// Second half: lane 0 of warp 0 spins until every block arrived, then the
+// block resolves the grid queue when it may be non-empty.
+__device__ __forceinline__ void sync_wait(const KParams& P, const KCtl& C, uint32_t t, SyncShared& sh,
+                                          double* s_gpos, double& snap_fit, uint32_t& snap_idx,
+                                          BarState& bs) {
+  const uint32_t tid = threadIdx.x;
+  const uint32_t cap = C.q_cap, qb = t % 3;
+  if (tid == 0) {
+    const uint64_t ts = globaltimer_ns();
+    unsigned long long v;
+    while (static_cast<uint32_t>(v = ld_acquire_gpu_u64(C.bar)) < bs.target) {
+      if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+    }
+    sh.need = static_cast<uint32_t>(v >> 32) != bs.appends;
+  }
+  __syncthreads();
+  if (sh.need) {  // block-uniform
+    __threadfence();
+    const uint32_t nq = __ldcg(&C.q_count[qb]);
+    if (tid == 0) bs.appends += nq;
+    if (nq) {
+      double wf;
+      uint32_t wi, ws;
+      resolve_queue(C, static_cast<size_t>(qb) * cap, nq, sh.rs, wf, wi, ws);
+      snap_fit = wf;
+      snap_idx = wi;
+      const size_t e = static_cast<size_t>(qb) * cap + ws;
+      for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.q_pos[e * P.d + a]);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    C.trace[t] = snap_fit;
+    C.trace_idx[t] = snap_idx;
+  }
+}
+
 template <class PosFn>
 __device__ __forceinline__ void sync_tail(const KParams& P, const KCtl& C, uint32_t t, SyncShared& sh,
                                           double* s_gpos, double& snap_fit, uint32_t& snap_idx,
@@ -928,24 +1002,17 @@ __global__ void __launch_bounds__(kResThreads, 1) k_sync_res(KParams P, KState S
   BarState bs;
   const uint32_t gbase = P.base + c0;
   auto pos_of = [&](uint32_t a, uint32_t i) { return sx[static_cast<size_t>(a) * chunk_cap + (i - gbase)]; };
+  // d = 1: the r1/r2 draws of a thread's first kPre particles for iteration
+  // t+1 depend on (t+1, particle) only, so they are computed while warp 0
+  // waits on the grid barrier of iteration t (the barrier latency hides
+  // behind ~60 Philox instructions per particle instead of idling).
+  constexpr int kPre = D == 1 ? 2 : 0;
+  double pre1[kPre > 0 ? kPre : 1], pre2[kPre > 0 ? kPre : 1];
+  bool have_pre = false;
   for (uint32_t t = t0; t < t1; ++t) {
     double bf = -INFINITY;
     uint32_t bi = kNoParticle, adm = 0;
-    for (uint32_t j = tid; j < m; j += blockDim.x) {
-      const uint32_t gi = gbase + j;
-      Fit<F> acc;
-      for (uint32_t a = 0; a < d; ++a) {
-        const size_t l = static_cast<size_t>(a) * chunk_cap + j;
-        const double r1 = uniform01(P, t, gi, a, 0);
-        const double r2 = uniform01(P, t, gi, a, 1);
-        const double x = sx[l];
-        const double nv = vel_step(P, sv[l], x, spb[l], s_gpos[a], r1, r2);
-        const double nx = pos_step(P, x, nv);
-        sv[l] = nv;
-        sx[l] = nx;
-        acc.add(nx, a);
-      }
-      const double f = acc.value();
+    auto finish = [&](uint32_t j, uint32_t gi, double f) {
       if (f > spbf[j]) {  // update_pbest (swarm.hpp:100-108)
         spbf[j] = f;
         for (uint32_t a = 0; a < d; ++a) {
@@ -960,10 +1027,64 @@ __global__ void __launch_bounds__(kResThreads, 1) k_sync_res(KParams P, KState S
           bi = gi;
         }
       }
+    };
+    uint32_t j = tid;
+    if constexpr (D == 1) {
+      auto one = [&](uint32_t jj, double r1, double r2) {
+        const double x = sx[jj];
+        const double nv = vel_step(P, sv[jj], x, spb[jj], s_gpos[0], r1, r2);
+        const double nx = pos_step(P, x, nv);
+        sv[jj] = nv;
+        sx[jj] = nx;
+        Fit<F> acc;
+        acc.add(nx, 0);
+        finish(jj, gbase + jj, acc.value());
+      };
+#pragma unroll
+      for (int k = 0; k < kPre; ++k, j += blockDim.x) {
+        if (j < m) {
+          const double r1 = have_pre ? pre1[k] : uniform01(P, t, gbase + j, 0, 0);
+          const double r2 = have_pre ? pre2[k] : uniform01(P, t, gbase + j, 0, 1);
+          one(j, r1, r2);
+        }
+      }
+      for (; j < m; j += blockDim.x) one(j, uniform01(P, t, gbase + j, 0, 0), uniform01(P, t, gbase + j, 0, 1));
+    } else {
+      for (; j < m; j += blockDim.x) {
+        const uint32_t gi = gbase + j;
+        Fit<F> acc;
+        for (uint32_t a = 0; a < d; ++a) {
+          const size_t l = static_cast<size_t>(a) * chunk_cap + j;
+          const double r1 = uniform01(P, t, gi, a, 0);
+          const double r2 = uniform01(P, t, gi, a, 1);
+          const double x = sx[l];
+          const double nv = vel_step(P, sv[l], x, spb[l], s_gpos[a], r1, r2);
+          const double nx = pos_step(P, x, nv);
+          sv[l] = nv;
+          sx[l] = nx;
+          acc.add(nx, a);
+        }
+        finish(j, gi, acc.value());
+      }
     }
     warp_publish(sh.bc, bf, bi, adm);
     __syncthreads();
-    sync_tail(P, C, t, sh, s_gpos, snap_fit, snap_idx, bs, pos_of);
+    uint32_t nq_block = 0;
+    sync_arrive(P, C, t, sh, bs, nq_block, pos_of);
+    if constexpr (kPre > 0) {
+      have_pre = t + 1 < t1;
+      if (have_pre) {
+        uint32_t jj = tid;
+#pragma unroll
+        for (int k = 0; k < kPre; ++k, jj += blockDim.x) {
+          if (jj < m) {
+            pre1[k] = uniform01(P, t + 1, gbase + jj, 0, 0);
+            pre2[k] = uniform01(P, t + 1, gbase + jj, 0, 1);
+          }
+        }
+      }
+    }
+    sync_wait(P, C, t, sh, s_gpos, snap_fit, snap_idx, bs);
   }
   for (uint32_t a = 0; a < d; ++a) {
     const size_t g = static_cast<size_t>(a) * P.ld + c0;

@@ -17,7 +17,8 @@ OUT = os.path.join(ROOT, "gpurun_out")
 
 # capture -> (workload, variant, iterations per captured launch, particles scale to the workload)
 CAPTURES = {
-    "cfg2_sync": ("cfg2", "cuda-sync", 200, 1.0, "k_sync<cubic> persistent, 2^20 x d=1, one launch = 200 iterations"),
+    "cfg2_sync": ("cfg2", "cuda-sync", 200, 1.0,
+                  "k_sync_res<cubic,1> SMEM-resident persistent, 2^20 x d=1, one launch = 200 iterations"),
     "cfg2_reduction_step": ("cfg2", "cuda-reduction", 1, 1.0, "k_classic_step<cubic,tree> (reduction phase 1), one iteration"),
     "cfg2_reduction_fold": ("cfg2", "cuda-reduction-fold", 1, 1.0, "k_classic_fold<tree> (reduction phase 2), one iteration"),
     "cfg3_async": ("cfg3", "cuda-async", 20, 1.0, "k_async<cubic>, 2^24 x d=1, one launch = 20 iterations"),
@@ -47,6 +48,8 @@ def main(tag):
             if rd is not None and wr is not None:
                 js.setdefault(wl, {})[var] = {
                     "dram_bytes_per_launch": (rd + wr) * scale, "iters_per_launch": iters,
+                    "warp_inst_per_launch": float(d["smsp__inst_executed.sum"][0].replace(",", "")) * scale
+                    if "smsp__inst_executed.sum" in d else None,
                     "dram_read": rd * scale, "dram_write": wr * scale,
                     "duration": dur, "capture": f"gpurun_out/{tag}_{key}.ncu-rep", "desc": desc}
             lines.append("")
