@@ -153,6 +153,7 @@ struct cupso_swarm {
   int sync_grid = 0;
   int step_cfg = 0;
   bool wave = false;
+  int wave_cfg = 0;
   bool res_checked = false;    // SMEM-resident cuda-sync probed
   int res_grid = 0;            // > 0: resident mode available (one block per SM)
   uint32_t res_cap = 0;        // particles per block chunk (SMEM rows)
@@ -197,7 +198,26 @@ using Cfg3 = StepCfg<1, 1, 6>;
 using Cfg4 = StepCfg<2, 0, 6>;
 using Cfg5 = StepCfg<1, 0, 6>;
 constexpr int kNumCfg = 6;
-using WaveCfg = StepCfg<1, 0, 8>;  // one particle per thread, 32 registers, 64 warps/SM
+// Wave-mode tunings: particles per thread, min blocks/SM, axes loaded together.
+using WaveCfg0 = StepCfg<1, 0, 8, 1>;  // one particle per thread, 32 registers, 64 warps/SM
+using WaveCfg1 = StepCfg<1, 0, 6, 2>;
+using WaveCfg2 = StepCfg<1, 0, 5, 4>;
+using WaveCfg3 = StepCfg<1, 0, 4, 4>;
+using WaveCfg4 = StepCfg<2, 0, 4, 2>;
+template <typename Fn>
+void dispatch_wave(int c, Fn&& fn) {
+  switch (c) {
+    case 1: fn(WaveCfg1{}); break;
+    case 2: fn(WaveCfg2{}); break;
+    case 3: fn(WaveCfg3{}); break;
+    case 4: fn(WaveCfg4{}); break;
+    default: fn(WaveCfg0{}); break;
+  }
+}
+int default_wave_cfg() {
+  if (const char* e = getenv("CUPSO_WAVE_CFG")) return atoi(e);
+  return 0;
+}
 
 template <typename Fn>
 void dispatch_cfg(int c, Fn&& fn) {
@@ -312,7 +332,10 @@ cupso_status ensure_queue(cupso_swarm* h, uint64_t cap) {
 
 // Wave mode of cuda-sync: [t0, t0+iters) as one CUDA graph of k_wave launches.
 cupso_status wave_graph(cupso_swarm* h, uint32_t t0, uint32_t iters, cudaGraphExec_t* out) {
-  const uint32_t blocks = static_cast<uint32_t>((h->P.n + kSyncThreads - 1) / kSyncThreads);
+  int np = 1;
+  dispatch_wave(h->wave_cfg, [&](auto WC) { np = decltype(WC)::kNP; });
+  const uint32_t units = static_cast<uint32_t>((h->P.n + np - 1) / np);
+  const uint32_t blocks = (units + kSyncThreads - 1) / kSyncThreads;
   TRY(ensure_queue(h, blocks));
   const auto key = std::make_tuple(100 + CUPSO_SYNC, t0, iters);
   auto it = h->graphs.find(key);
@@ -328,12 +351,15 @@ cupso_status wave_graph(cupso_swarm* h, uint32_t t0, uint32_t iters, cudaGraphEx
   cudaError_t le = cudaSuccess;
   dispatch_fit(h->fid, [&](auto F) {
     constexpr int f = decltype(F)::value;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_wave<f, WaveCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (uint32_t t = t0; t < t0 + iters && le == cudaSuccess; ++t) {
-      k_wave<f, WaveCfg><<<blocks, kSyncThreads, smem, h->stream>>>(h->P, h->S, h->C, t);
-      le = cudaGetLastError();
-    }
+    dispatch_wave(h->wave_cfg, [&](auto WC) {
+      using W = decltype(WC);
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_wave<f, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      for (uint32_t t = t0; t < t0 + iters && le == cudaSuccess; ++t) {
+        k_wave<f, W><<<blocks, kSyncThreads, smem, h->stream>>>(h->P, h->S, h->C, t);
+        le = cudaGetLastError();
+      }
+    });
   });
   cudaError_t ee = cudaStreamEndCapture(h->stream, &g);
   CK(le);
@@ -581,6 +607,11 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   return CUPSO_OK;
 }
 
+// aux slots serve the classic engines' per-group winners and init_swarm's
+// block argmax (at most kInitArgmaxBlocks blocks)
+constexpr uint32_t kInitArgmaxBlocks = 1024;
+uint64_t aux_entries(const cupso_swarm* h) { return std::max<uint64_t>(h->groups, kInitArgmaxBlocks) + 1; }
+
 cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int device, uint32_t first,
                          uint32_t count, cupso_swarm** out) {
   if (!out) return fail(CUPSO_EINVAL, "null output handle");
@@ -621,6 +652,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   key_schedule(seed, P);
   h->step_cfg = default_step_cfg(P);
   h->wave = use_wave(P);
+  h->wave_cfg = default_wave_cfg();
   h->groups = (count + p->group_size - 1) / p->group_size;
   h->rec_bytes = sizeof(Rec) + sizeof(double) * p->dims;
   h->is_async.assign(h->T, 0);
@@ -647,8 +679,8 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   void *c, *tr, *ti, *adm, *tk, *af, *ai, *rall;
   if ((st = dmalloc(h, &c, ctl)) || (st = dmalloc(h, &tr, h->T * 8ull)) ||
       (st = dmalloc(h, &ti, h->T * 4ull)) || (st = dmalloc(h, &adm, h->T * 8ull)) ||
-      (st = dmalloc(h, &tk, h->T * 8ull)) || (st = dmalloc(h, &af, h->groups * 8ull + 8)) ||
-      (st = dmalloc(h, &ai, h->groups * 4ull + 4)))
+      (st = dmalloc(h, &tk, h->T * 8ull)) || (st = dmalloc(h, &af, aux_entries(h) * 8ull)) ||
+      (st = dmalloc(h, &ai, aux_entries(h) * 4ull)))
     return bail(st);
   (void)rall;
   h->ctl_block = static_cast<unsigned char*>(c);
@@ -686,22 +718,9 @@ cupso_status init_impl(cupso_swarm* h) {
     e = cudaGetLastError();
   });
   CK(e);
-  const uint32_t nb = static_cast<uint32_t>(std::min<uint64_t>((h->P.n + 255) / 256, 1024));
-  // aux arrays hold >= groups entries; use a dedicated scratch when nb exceeds them
-  double* af = h->C.aux_fit;
-  uint32_t* ai = h->C.aux_idx;
-  void *saf = nullptr, *sai = nullptr;
-  if (nb > h->groups) {
-    CK(cudaMalloc(&saf, nb * 8));
-    CK(cudaMalloc(&sai, nb * 4));
-    af = static_cast<double*>(saf);
-    ai = static_cast<uint32_t*>(sai);
-  }
-  k_argmax_blocks<<<nb, 256, 0, h->stream>>>(h->P, h->S.pbf, af, ai);
-  KCtl c2 = h->C;
-  c2.aux_fit = af;
-  c2.aux_idx = ai;
-  k_argmax_final<<<1, 1024, 0, h->stream>>>(h->P, h->S, c2, nb);
+  const uint32_t nb = static_cast<uint32_t>(std::min<uint64_t>((h->P.n + 255) / 256, kInitArgmaxBlocks));
+  k_argmax_blocks<<<nb, 256, 0, h->stream>>>(h->P, h->S.pbf, h->C.aux_fit, h->C.aux_idx);
+  k_argmax_final<<<1, 1024, 0, h->stream>>>(h->P, h->S, h->C, nb);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(h->C.admitted, 0, h->T * 8ull, h->stream));
   CK(cudaMemsetAsync(h->C.trace_key, 0, h->T * 8ull, h->stream));
@@ -719,8 +738,6 @@ cupso_status init_impl(cupso_swarm* h) {
   Rec r;
   CK(cudaMemcpyAsync(&r, h->C.snap, sizeof r, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  if (saf) cudaFree(saf);
-  if (sai) cudaFree(sai);
   h->initial_fit = r.fit;
   h->initial_particle = r.particle;
   h->t = 0;

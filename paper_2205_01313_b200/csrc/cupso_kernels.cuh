@@ -502,11 +502,12 @@ __device__ __forceinline__ void warp_publish(BlockCand& bc, double bf, uint32_t 
 // Tunings of the fused step: particles per thread-item (1: scalar LDG.64,
 // 2: LDG.128 over two adjacent particles), software prefetch of the next
 // item's loads, and the occupancy target handed to __launch_bounds__.
-template <int NP_, int PF_, int MINB_>
+template <int NP_, int PF_, int MINB_, int KD_ = 1>
 struct StepCfg {
   static constexpr int kNP = NP_;
   static constexpr int kPF = PF_;
   static constexpr int kMinBlocks = MINB_;
+  static constexpr int kKD = KD_;  // axes whose loads are issued together (memory-level parallelism)
 };
 
 template <int NP>
@@ -555,23 +556,37 @@ __device__ __forceinline__ void step_items(const KParams& P, const KState& S, ui
       const uint32_t li = NP * u;
       const uint32_t g0 = P.base + li;
       Fit<F> acc[NP];
-      for (uint32_t a = 0; a < P.d; ++a) {
-        const size_t at = static_cast<size_t>(a) * P.ld + li;
-        double x[NP], v[NP], pb[NP], nx[NP], nv[NP];
-        ldv<NP>(S.pos + at, x);
-        ldv<NP>(S.vel + at, v);
-        ldv<NP>(S.pb + at, pb);
-        const double g = gpos[a];
+      constexpr int KD = CFG::kKD;
+      for (uint32_t a0 = 0; a0 < P.d; a0 += KD) {
+        // issue the loads of KD axes before any of their compute
+        double x[KD][NP], v[KD][NP], pb[KD][NP];
 #pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const double r1 = uniform01(P, t, g0 + k, a, 0);
-          const double r2 = uniform01(P, t, g0 + k, a, 1);
-          nv[k] = vel_step(P, v[k], x[k], pb[k], g, r1, r2);
-          nx[k] = pos_step(P, x[k], nv[k]);
-          acc[k].add(nx[k], a);
+        for (int q = 0; q < KD; ++q) {
+          if (KD == 1 || a0 + q < P.d) {
+            const size_t at = static_cast<size_t>(a0 + q) * P.ld + li;
+            ldv<NP>(S.pos + at, x[q]);
+            ldv<NP>(S.vel + at, v[q]);
+            ldv<NP>(S.pb + at, pb[q]);
+          }
         }
-        stv<NP>(S.vel + at, nv);
-        stv<NP>(S.pos + at, nx);
+#pragma unroll
+        for (int q = 0; q < KD; ++q) {
+          if (KD > 1 && a0 + q >= P.d) break;
+          const uint32_t a = a0 + q;
+          const size_t at = static_cast<size_t>(a) * P.ld + li;
+          const double g = gpos[a];
+          double nx[NP], nv[NP];
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            const double r1 = uniform01(P, t, g0 + k, a, 0);
+            const double r2 = uniform01(P, t, g0 + k, a, 1);
+            nv[k] = vel_step(P, v[q][k], x[q][k], pb[q][k], g, r1, r2);
+            nx[k] = pos_step(P, x[q][k], nv[k]);
+            acc[k].add(nx[k], a);
+          }
+          stv<NP>(S.vel + at, nv);
+          stv<NP>(S.pos + at, nx);
+        }
       }
       double pbf[NP];
       ldv<NP>(S.pbf + li, pbf);
