@@ -154,6 +154,10 @@ struct cupso_swarm {
   int step_cfg = 0;
   bool wave = false;
   int wave_cfg = 0;
+  bool tile_checked = false;   // tiled cuda-async probed
+  uint32_t tile_cap = 0;       // > 0: tiled async available (particles per SMEM tile)
+  size_t tile_smem = 0;
+  int tile_grid = 0, tile_k = 8;
   bool res_checked = false;    // SMEM-resident cuda-sync probed
   int res_grid = 0;            // > 0: resident mode available (one block per SM)
   uint32_t res_cap = 0;        // particles per block chunk (SMEM rows)
@@ -493,8 +497,76 @@ cupso_status launch_resident(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   return CUPSO_OK;
 }
 
+// Tiled (temporally blocked) mode of cuda-async: two 512-thread blocks per SM,
+// each cycling SMEM tiles of its particle chunk through K iterations at a
+// time. Used when the swarm is larger than what SMEM holds at once (otherwise
+// plain k_async is already L2/SMEM friendly). CUPSO_ASYNC_MODE=plain|tiled and
+// CUPSO_ASYNC_K override.
+template <int F>
+const void* tiled_kernel(uint32_t d) {
+  return d == 1 ? reinterpret_cast<const void*>(k_async_tiled<F, 1>)
+                : reinterpret_cast<const void*>(k_async_tiled<F, 0>);
+}
+
+bool tiled_fits(cupso_swarm* h) {
+  if (h->tile_checked) return h->tile_cap > 0;
+  h->tile_checked = true;
+  const char* mode = getenv("CUPSO_ASYNC_MODE");
+  if (mode && !strcmp(mode, "plain")) return false;
+  const double state_bytes = static_cast<double>(h->P.ld) * (3.0 * h->P.d + 1.0) * 8.0;
+  if (!(mode && !strcmp(mode, "tiled")) && state_bytes <= 64.0 * (1 << 20)) return false;
+  int per_sm_smem = 0;
+  if (cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device) != cudaSuccess)
+    return false;
+  const uint64_t dpad = (h->P.d + 1ull) & ~1ull;
+  bool ok = false;
+  uint64_t cap = 0, dyn = 0;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    const void* kfn = tiled_kernel<f>(h->P.d);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kfn) != cudaSuccess) return;
+    const int64_t budget = per_sm_smem / 2 - static_cast<int64_t>(fa.sharedSizeBytes) - 1024;
+    if (budget <= 0) return;
+    cap = (static_cast<uint64_t>(budget) / sizeof(double) - dpad) / (3ull * h->P.d + 1ull);
+    cap = cap / 32 * 32;
+    if (cap < static_cast<uint64_t>(kTileThreads)) return;
+    dyn = (dpad + (3ull * h->P.d + 1ull) * cap) * sizeof(double);
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)) != cudaSuccess)
+      return;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTileThreads, dyn) != cudaSuccess) return;
+    ok = per_sm >= 2;
+  });
+  cudaGetLastError();
+  if (!ok) return false;
+  h->tile_cap = static_cast<uint32_t>(cap);
+  h->tile_smem = static_cast<size_t>(dyn);
+  h->tile_grid = 2 * num_sms(h->device);
+  const char* k = getenv("CUPSO_ASYNC_K");
+  // K = 32: tile load/store amortised to ~2 B per particle-update (2^24 x d=1:
+  // 121 us/iteration vs 157 at K = 8 and 141 for plain k_async; B200, round 1)
+  h->tile_k = k ? std::max(1, atoi(k)) : 32;
+  return true;
+}
+
+cupso_status launch_tiled(cupso_swarm* h, uint32_t t0, uint32_t t1) {
+  CK(cudaMemsetAsync(h->C.seq, 0, sizeof(uint32_t), h->stream));
+  cudaError_t e = cudaSuccess;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    uint32_t cap = h->tile_cap, K = static_cast<uint32_t>(h->tile_k);
+    void* args[] = {&h->P, &h->S, &h->C, &t0, &t1, &cap, &K};
+    e = cudaLaunchKernel(tiled_kernel<f>(h->P.d), dim3(h->tile_grid), dim3(kTileThreads), args, h->tile_smem,
+                         h->stream);
+  });
+  CK(e);
+  return CUPSO_OK;
+}
+
 cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_t t1) {
   if (variant == CUPSO_SYNC && resident_fits(h)) return launch_resident(h, t0, t1);
+  if (variant == CUPSO_ASYNC && tiled_fits(h)) return launch_tiled(h, t0, t1);
   TRY(ensure_sync_grid(h));
   const size_t smem = sync_smem(h);
   cudaError_t e = cudaSuccess;
@@ -579,6 +651,7 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
     CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
   }
   if (iters && variant == CUPSO_SYNC && !wave && !h->comm) resident_fits(h);  // probe outside the timed region
+  if (iters && variant == CUPSO_ASYNC) tiled_fits(h);
   if (iters && ((variant == CUPSO_SYNC && !wave) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
   CK(cudaEventRecord(h->ev0, h->stream));
   if (iters) {

@@ -1368,108 +1368,252 @@ __global__ void k_adopt(KParams P, KCtl C, const unsigned char* records, uint32_
 // a seqlock: readers retry on an odd or changed version; a writer takes the
 // record with CAS(version: even -> odd), re-checks beats() under it, writes,
 // and releases with version+2. No grid barrier anywhere.
+constexpr int kTileThreads = 512;
+
+struct AsyncShared {
+  double fit;
+  uint32_t idx, ver, have, ok;
+};
+
+// Consistent (torn-read-free) copy of the live record into s_gpos / as.fit;
+// the position copy is skipped while the version is unchanged. All threads call.
+__device__ __forceinline__ void async_read_gbest(const KParams& P, const KCtl& C, double* s_gpos,
+                                                 AsyncShared& as) {
+  const uint32_t tid = threadIdx.x;
+  const uint64_t ts = globaltimer_ns();
+  for (;;) {
+    __syncthreads();  // previous round's readers are done with as.ok / as.have
+    if (tid == 0) {
+      const uint32_t v = ld_acquire_gpu(C.seq);
+      as.ok = (v & 1u) == 0u;
+      as.have = 1;  // unchanged since our last copy
+      if (as.ok && v != as.ver) {
+        as.have = 2;  // needs a copy
+        as.ver = v;
+      }
+      if (!as.ok && globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+    }
+    __syncthreads();
+    if (!as.ok) continue;
+    if (as.have == 1) break;
+    for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.live_pos[a]);
+    if (tid == 0) {
+      as.fit = __ldcg(&C.live->fit);
+      as.idx = __ldcg(&C.live->particle);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const uint32_t v2 = ld_acquire_gpu(C.seq);
+      as.ok = v2 == as.ver;
+      if (!as.ok) as.ver = 0xffffffffu;
+    }
+    __syncthreads();
+    if (as.ok) break;
+  }
+}
+
+// Warp 0 publishes the block winner into the live record when it beats it
+// (lock-free pre-check, then CAS(version even->odd), re-check, write, release
+// version+2) and folds its view of the gbest into trace_key[t].
+template <class PosFn>
+__device__ __forceinline__ void async_commit(const KParams& P, const KCtl& C, uint32_t t, BlockCand& bc,
+                                             double snap_fit, PosFn pos_of) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp != 0) return;
+  const uint32_t nq = bc.n;
+  double view = snap_fit;
+  if (nq) {
+    double f = lane < nq ? bc.f[lane] : -INFINITY;
+    uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
+    warp_argmax(f, i);
+    // lane 0 decides for the whole warp: per-lane loads of a record that other
+    // blocks are writing may disagree, and the warp must take one branch
+    double lf0 = 0.0;
+    int try_lock = 0;
+    if (lane == 0) {
+      lf0 = ld_acquire_gpu_f64(&C.live->fit);
+      try_lock = may_beat(C.live, f, i);
+    }
+    lf0 = __shfl_sync(0xffffffffu, lf0, 0);
+    try_lock = __shfl_sync(0xffffffffu, try_lock, 0);
+    if (try_lock) {
+      uint32_t v = 0;
+      double lf = 0.0;
+      uint32_t lp = 0;
+      if (lane == 0) {
+        const uint64_t tl = globaltimer_ns();
+        for (;;) {
+          v = ld_acquire_gpu(C.seq);
+          if (!(v & 1u) && atomicCAS(C.seq, v, v + 1u) == v) break;
+          if (globaltimer_ns() - tl > kSpinTimeoutNs) __trap();
+        }
+        __threadfence();
+        lf = __ldcg(&C.live->fit);
+        lp = __ldcg(&C.live->particle);
+      }
+      v = __shfl_sync(0xffffffffu, v, 0);
+      lf = __shfl_sync(0xffffffffu, lf, 0);
+      lp = __shfl_sync(0xffffffffu, lp, 0);
+      if (beats(f, i, lf, lp)) {
+        for (uint32_t a = lane; a < P.d; a += 32) C.live_pos[a] = pos_of(a, i);
+        __syncwarp();
+        if (lane == 0) write_rec(C.live, f, i);
+        view = f;
+      } else {
+        view = lf;
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(C.seq, v + 2u);
+    } else {
+      view = lf0 > view ? lf0 : view;
+    }
+  }
+  if (lane == 0) {
+    if (bc.adm) atomicAdd(&C.admitted[t], bc.adm);
+    atomicMax(&C.trace_key[t], order_key(view));
+    bc.n = 0;
+    bc.adm = 0;
+  }
+}
+
 template <int F, class CFG>
 __global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_async(KParams P, KState S, KCtl C, uint32_t t0,
                                                         uint32_t t1) {
   extern __shared__ double s_gpos[];
   __shared__ BlockCand bc;
-  __shared__ double s_fit;
-  __shared__ uint32_t s_idx, s_ver, s_have, s_ok;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    s_have = 0;
-    s_ver = 0xffffffffu;
+  __shared__ AsyncShared as;
+  if (threadIdx.x == 0) {
+    as.have = 0;
+    as.ver = 0xffffffffu;
     bc.n = 0;
     bc.adm = 0;
   }
   __syncthreads();
+  auto pos_of = [&](uint32_t a, uint32_t i) { return S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)]; };
   for (uint32_t t = t0; t < t1; ++t) {
-    // consistent read of the live record (skip the position copy when unchanged)
-    const uint64_t ts = globaltimer_ns();
-    for (;;) {
-      __syncthreads();  // previous round's readers are done with s_ok / s_have
-      if (tid == 0) {
-        const uint32_t v = ld_acquire_gpu(C.seq);
-        s_ok = (v & 1u) == 0u;
-        s_have = 1;  // unchanged since our last copy
-        if (s_ok && v != s_ver) {
-          s_have = 2;  // needs a copy
-          s_ver = v;
-        }
-        if (!s_ok && globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
-      }
-      __syncthreads();
-      if (!s_ok) continue;
-      if (s_have == 1) break;
-      for (uint32_t a = tid; a < P.d; a += blockDim.x) s_gpos[a] = __ldcg(&C.live_pos[a]);
-      if (tid == 0) {
-        s_fit = __ldcg(&C.live->fit);
-        s_idx = __ldcg(&C.live->particle);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        const uint32_t v2 = ld_acquire_gpu(C.seq);
-        s_ok = v2 == s_ver;
-        if (!s_ok) s_ver = 0xffffffffu;
-      }
-      __syncthreads();
-      if (s_ok) break;
-    }
-    const double snap_fit = s_fit;
+    async_read_gbest(P, C, s_gpos, as);
+    const double snap_fit = as.fit;
     double bf;
     uint32_t bi, adm;
     step_items<F, CFG>(P, S, t, s_gpos, snap_fit, bf, bi, adm);
     warp_publish(bc, bf, bi, adm);
     __syncthreads();
-    if (warp == 0) {
-      const uint32_t nq = bc.n;
-      double view = snap_fit;
-      if (nq) {
-        double f = lane < nq ? bc.f[lane] : -INFINITY;
-        uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
-        warp_argmax(f, i);
-        // lock-free pre-check (may_beat); re-checked under the CAS
-        const double lf0 = ld_acquire_gpu_f64(&C.live->fit);
-        if (may_beat(C.live, f, i)) {
-          uint32_t v = 0;
-          if (lane == 0) {
-            const uint64_t tl = globaltimer_ns();
-            for (;;) {
-              v = ld_acquire_gpu(C.seq);
-              if (!(v & 1u) && atomicCAS(C.seq, v, v + 1u) == v) break;
-              if (globaltimer_ns() - tl > kSpinTimeoutNs) __trap();
-            }
-            __threadfence();
-          }
-          v = __shfl_sync(0xffffffffu, v, 0);
-          const double lf = __ldcg(&C.live->fit);
-          const uint32_t lp = __ldcg(&C.live->particle);
-          const bool win = beats(f, i, lf, lp);
-          if (win) {
-            for (uint32_t a = lane; a < P.d; a += 32)
-              C.live_pos[a] = S.pos[static_cast<size_t>(a) * P.ld + (i - P.base)];
-            __syncwarp();
-            if (lane == 0) write_rec(C.live, f, i);
-            view = f;
-          } else {
-            view = lf;
-          }
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) st_release_gpu(C.seq, v + 2u);
-        } else {
-          view = lf0 > view ? lf0 : view;
+    async_commit(P, C, t, bc, snap_fit, pos_of);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------- async, tiled
+// Temporal blocking for the asynchronous variant. Asynchronous PSO lets each
+// particle advance at its own pace against the latest published gbest, so a
+// block may keep a tile of its particles in SMEM and run K iterations on it
+// before writing it back and loading the next tile. Every particle still does
+// exactly T iterations with draws keyed by its own (t, particle, axis); HBM
+// traffic drops from (5d+1)*8 B per particle-update to ~(8d+2)*8/K B and the
+// kernel becomes issue-bound. Each tile-iteration re-reads the live record
+// through the seqlock (skipping the copy when unchanged) and publishes
+// improvements with the same CAS protocol as k_async.
+template <int F, int D = 0>
+__global__ void __launch_bounds__(kTileThreads, 2) k_async_tiled(KParams P, KState S, KCtl C, uint32_t t0,
+                                                                 uint32_t t1, uint32_t tile_cap, uint32_t K) {
+  extern __shared__ double smem[];
+  __shared__ BlockCand bc;
+  __shared__ AsyncShared as;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t d = D > 0 ? static_cast<uint32_t>(D) : P.d;
+  const uint32_t c0 = static_cast<uint32_t>(static_cast<uint64_t>(P.n) * blockIdx.x / gridDim.x);
+  const uint32_t c1 = static_cast<uint32_t>(static_cast<uint64_t>(P.n) * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t dpad = (d + 1u) & ~1u;
+  double* s_gpos = smem;
+  double* sx = smem + dpad;
+  double* sv = sx + static_cast<size_t>(d) * tile_cap;
+  double* spb = sv + static_cast<size_t>(d) * tile_cap;
+  double* spbf = spb + static_cast<size_t>(d) * tile_cap;
+  if (tid == 0) {
+    as.have = 0;
+    as.ver = 0xffffffffu;
+    bc.n = 0;
+    bc.adm = 0;
+  }
+  __syncthreads();
+  for (uint32_t tb = t0; tb < t1; tb += K) {
+    const uint32_t te = tb + K < t1 ? tb + K : t1;
+    for (uint32_t s0 = c0; s0 < c1; s0 += tile_cap) {
+      const uint32_t m = (c1 - s0) < tile_cap ? (c1 - s0) : tile_cap;
+      for (uint32_t a = 0; a < d; ++a) {
+        const size_t g = static_cast<size_t>(a) * P.ld + s0;
+        const size_t l = static_cast<size_t>(a) * tile_cap;
+        for (uint32_t j = tid; j < m; j += blockDim.x) {
+          sx[l + j] = S.pos[g + j];
+          sv[l + j] = S.vel[g + j];
+          spb[l + j] = S.pb[g + j];
         }
       }
-      if (lane == 0) {
-        if (bc.adm) atomicAdd(&C.admitted[t], bc.adm);
-        atomicMax(&C.trace_key[t], order_key(view));
-        bc.n = 0;
-        bc.adm = 0;
+      for (uint32_t j = tid; j < m; j += blockDim.x) spbf[j] = S.pbf[s0 + j];
+      const uint32_t gbase = P.base + s0;
+      auto pos_of = [&](uint32_t a, uint32_t i) { return sx[static_cast<size_t>(a) * tile_cap + (i - gbase)]; };
+      async_read_gbest(P, C, s_gpos, as);  // also orders the tile load before use
+      for (uint32_t t = tb; t < te; ++t) {
+        // The version check for the *next* tile-iteration is issued now and
+        // consumed after the compute, so its L2 latency overlaps the work; the
+        // gbest used here may be one tile-iteration stale (asynchronous PSO).
+        uint32_t ver_now = 0;
+        if (tid == 0) ver_now = ld_acquire_gpu(C.seq);
+        const double snap_fit = as.fit;
+        double bf = -INFINITY;
+        uint32_t bi = kNoParticle, adm = 0;
+        for (uint32_t j = tid; j < m; j += blockDim.x) {
+          const uint32_t gi = gbase + j;
+          Fit<F> acc;
+          for (uint32_t a = 0; a < d; ++a) {
+            const size_t l = static_cast<size_t>(a) * tile_cap + j;
+            const double r1 = uniform01(P, t, gi, a, 0);
+            const double r2 = uniform01(P, t, gi, a, 1);
+            const double x = sx[l];
+            const double nv = vel_step(P, sv[l], x, spb[l], s_gpos[a], r1, r2);
+            const double nx = pos_step(P, x, nv);
+            sv[l] = nv;
+            sx[l] = nx;
+            acc.add(nx, a);
+          }
+          const double f = acc.value();
+          if (f > spbf[j]) {
+            spbf[j] = f;
+            for (uint32_t a = 0; a < d; ++a) {
+              const size_t l = static_cast<size_t>(a) * tile_cap + j;
+              spb[l] = sx[l];
+            }
+          }
+          if (f > snap_fit) {
+            ++adm;
+            if (beats(f, gi, bf, bi)) {
+              bf = f;
+              bi = gi;
+            }
+          }
+        }
+        warp_publish(bc, bf, bi, adm);
+        if (tid == 0) as.have = ver_now != as.ver ? 2u : 1u;  // 2: the live record moved
+        __syncthreads();
+        if (tid == 0 && bc.n) as.have = 2u;  // publishing: re-read the record afterwards
+        async_commit(P, C, t, bc, snap_fit, pos_of);
+        __syncthreads();
+        if (as.have == 2) async_read_gbest(P, C, s_gpos, as);  // block-uniform
       }
+      for (uint32_t a = 0; a < d; ++a) {
+        const size_t g = static_cast<size_t>(a) * P.ld + s0;
+        const size_t l = static_cast<size_t>(a) * tile_cap;
+        for (uint32_t j = tid; j < m; j += blockDim.x) {
+          S.pos[g + j] = sx[l + j];
+          S.vel[g + j] = sv[l + j];
+          S.pb[g + j] = spb[l + j];
+        }
+      }
+      for (uint32_t j = tid; j < m; j += blockDim.x) S.pbf[s0 + j] = spbf[j];
+      __syncthreads();  // the next tile overwrites SMEM
     }
-    __syncthreads();
   }
 }
 
