@@ -129,7 +129,12 @@ def test_async_statistics_32_seeds(cupso):
     assert np.median(-asy) < 1.0
 
 
-def test_async_invariants(cupso, oracle):
+@pytest.mark.parametrize("mode", ["plain", "tiled"])
+def test_async_invariants(cupso, oracle, monkeypatch, mode):
+    """Both async schedules (free-running blocks; SMEM tiles advanced K iterations
+    at a time) keep a consistent, monotone global best."""
+    monkeypatch.setenv("CUPSO_ASYNC_MODE", mode)
+    monkeypatch.setenv("CUPSO_ASYNC_K", "5")
     f = cupso.find_fitness("cubic")
     p = cupso.make_params(f, 100000, 3, 80)
     with cupso.Swarm(p, f, 2) as sw:
