@@ -21,8 +21,8 @@ CAPTURES = {
                   "k_sync_res<cubic,1> SMEM-resident persistent, 2^20 x d=1, one launch = 200 iterations"),
     "cfg2_reduction_step": ("cfg2", "cuda-reduction", 1, 1.0, "k_classic_step<cubic,tree> (reduction phase 1), one iteration"),
     "cfg2_reduction_fold": ("cfg2", "cuda-reduction-fold", 1, 1.0, "k_classic_fold<tree> (reduction phase 2), one iteration"),
-    "cfg3_async": ("cfg3", "cuda-async", 20, 1.0, "k_async<cubic>, 2^24 x d=1, one launch = 20 iterations"),
-    "cfg4_wave": ("cfg4", "cuda-sync", 1, 1.0, "k_wave<rastrigin>, 2^20 x d=32, one iteration (iteration 5)"),
+    "cfg3_async": ("cfg3", "cuda-async", 64, 1.0, "k_async_tiled<cubic,1> (SMEM tiles, K=32), 2^24 x d=1, one launch = 64 iterations"),
+    "cfg4_wave": ("cfg4", "cuda-sync", 1, 1.0, "k_wave<rastrigin> (cos_pso), 2^20 x d=32, one iteration (iteration 5)"),
     "cfg5proxy_wave": ("cfg5", "cuda-sync", 1, 16.0, "k_wave<sphere>, 2^24 x d=8 proxy of 2^28 (x16 per launch), iteration 5"),
 }
 
