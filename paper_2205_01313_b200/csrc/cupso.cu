@@ -631,6 +631,13 @@ cupso_status sharded_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
 cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* seconds) {
   if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
   if (variant < 0 || variant >= kNumVar) return fail(CUPSO_EINVAL, "unknown variant %d", variant);
+  // The fused kernels stage the gbest position in SMEM (<= kMaxSyncDims axes).
+  // Wider swarms run the same synchronous algorithm as the classic fused
+  // queue-lock launches, which read it from global memory -- bit-identical.
+  if ((variant == CUPSO_SYNC || variant == CUPSO_ASYNC) && h->P.d > kMaxSyncDims) {
+    if (h->comm) return fail(CUPSO_EINVAL, "sharded cuda-sync: dims (%u) above %u", h->P.d, kMaxSyncDims);
+    variant = CUPSO_QUEUE_LOCK;
+  }
   if (!h->initialized) return fail(CUPSO_ELOGIC, "cupso_step before cupso_init");
   if (static_cast<uint64_t>(h->t) + iters > h->T)
     return fail(CUPSO_EINVAL, "cupso_step: %u + %u iterations exceed max_iter (%u)", h->t, iters, h->T);

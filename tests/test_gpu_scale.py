@@ -182,6 +182,18 @@ def test_group_size_one_and_large(cupso, oracle):
         cupso.find_engine("cuda-reduction").run(cupso.make_params(f, 24, 2, 4, 2048), f, cupso.rng_key(3))
 
 
+def test_very_wide_swarm(cupso, oracle):
+    """d above the fused kernels' SMEM snapshot (12288 axes) still runs and still
+    matches serial bit for bit (falls back to the classic fused launches)."""
+    f = cupso.find_fitness("sphere")
+    n, d, T = 64, 13000, 3
+    p = cupso.make_params(f, n, d, T)
+    ref = oracle.run_serial("sphere", n, d, T, 4, want_state=False)
+    for e in ("cuda-sync", "cuda-reduction"):
+        r = cupso.find_engine(e).run(p, f, cupso.rng_key(4))
+        assert same(r.trace, ref.trace) and same(r.gbest_pos, ref.gbest_pos), e
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2**32, 2**64 - 1])
 def test_extreme_seeds(cupso, oracle, seed):
     f = cupso.find_fitness("sphere")
