@@ -23,6 +23,7 @@
 
 #include "../../include/cupso.h"
 #include "cupso_kernels.cuh"
+#include "cupso_spec.cuh"
 
 using namespace cupso;
 
@@ -163,6 +164,13 @@ struct cupso_swarm {
   uint32_t res_cap = 0;        // particles per block chunk (SMEM rows)
   size_t res_smem = 0;
   uint32_t q_alloc = 0;
+  bool spec_checked = false;   // speculative temporally-blocked cuda-sync probed
+  int spec_grid = 0;           // > 0: spec mode available
+  KState S_alt{};              // the pass's write buffer (ping-pong with S)
+  SpecCtl* spec_ctl = nullptr; // device pass schedule
+  SpecCtl* spec_host = nullptr;  // pinned mirror
+  uint32_t spec_kmax = 64;
+  uint64_t spec_passes = 0, spec_fails = 0;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
   std::vector<uint8_t> is_async;
   std::map<std::tuple<int, uint32_t, uint32_t>, cudaGraphExec_t> graphs;
@@ -564,6 +572,136 @@ cupso_status launch_tiled(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   return CUPSO_OK;
 }
 
+// Speculative temporally-blocked mode of cuda-sync (cupso_spec.cuh): each
+// pass keeps every particle in registers for K iterations against a fixed
+// snapshot and is re-run exactly when an admission falsifies it. Available
+// for dims 1/2/4/8 (the particle's state must fit in registers); needs a second
+// state buffer. CUPSO_SYNC_MODE selects another mode; CUPSO_SPEC_K caps K.
+// (particles per thread unit, min blocks/SM) per dims: the whole particle
+// state plus two Philox streams per axis must stay in registers (no spills,
+// ptxas.log); the cos-based fitnesses need a few more.
+template <int F, int D>
+struct SpecKernel {
+  static constexpr int kNP = D == 1 ? 4 : (D == 2 ? 2 : 1);
+  static constexpr int kMinB = D == 8 || D == 1 ? 2 : (F >= kGriewank ? 2 : 3);
+  static const void* fn() { return reinterpret_cast<const void*>(k_spec<F, D, kNP, kMinB>); }
+};
+
+// Alternative (NP, MINB) tunings for the BASELINE dims, selected with
+// CUPSO_SPEC_CFG=<n> (exploration; 0 = the default above).
+template <int F>
+const void* spec_kernel_alt(uint32_t d, int cfg, int* np) {
+  if (d == 1) {
+    switch (cfg) {
+      case 1: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 1, 1, 4>);
+      case 2: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 1, 1, 6>);
+      case 3: *np = 2; return reinterpret_cast<const void*>(k_spec<F, 1, 2, 4>);
+      case 5: *np = 4; return reinterpret_cast<const void*>(k_spec<F, 1, 4, 3>);
+      case 6: *np = 8; return reinterpret_cast<const void*>(k_spec<F, 1, 8, 1>);
+      case 4: *np = 2; return reinterpret_cast<const void*>(k_spec<F, 1, 2, 6>);
+    }
+  } else if (d == 8) {
+    switch (cfg) {
+      case 1: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 8, 1, 3>);
+      case 2: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 8, 1, 1>);
+    }
+  }
+  return nullptr;
+}
+
+template <int F>
+const void* spec_kernel(uint32_t d, int* np) {
+  if (const char* e = getenv("CUPSO_SPEC_CFG"))
+    if (const void* k = spec_kernel_alt<F>(d, atoi(e), np)) return k;
+  switch (d) {
+    case 1: *np = SpecKernel<F, 1>::kNP; return SpecKernel<F, 1>::fn();
+    case 2: *np = SpecKernel<F, 2>::kNP; return SpecKernel<F, 2>::fn();
+    case 4: *np = SpecKernel<F, 4>::kNP; return SpecKernel<F, 4>::fn();
+    case 8: *np = SpecKernel<F, 8>::kNP; return SpecKernel<F, 8>::fn();
+    default: return nullptr;
+  }
+}
+
+bool spec_fits(cupso_swarm* h) {
+  if (h->spec_checked) return h->spec_grid > 0;
+  h->spec_checked = true;
+  if (h->comm) return false;
+  if (const char* e = getenv("CUPSO_SYNC_MODE"))
+    if (strcmp(e, "spec") != 0 && strcmp(e, "auto") != 0) return false;
+  const void* kfn = nullptr;
+  int np = 1;
+  dispatch_fit(h->fid, [&](auto F) { kfn = spec_kernel<decltype(F)::value>(h->P.d, &np); });
+  if (!kfn) return false;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kSyncThreads, 0) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  // balanced grid: every thread takes the same number of units
+  const uint64_t units = (h->P.n + np - 1ull) / np;
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
+  const uint64_t rounds = (units + resident - 1) / resident;
+  const uint64_t threads = (units + rounds - 1) / rounds;
+  const uint64_t grid = std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads);
+  // second state buffer (the pass writes B while A stays intact for a re-run)
+  const size_t cells = h->P.ld * h->P.d;
+  void *pos = nullptr, *vel = nullptr, *pb = nullptr, *pbf = nullptr, *ctl = nullptr, *host = nullptr;
+  if (cudaMalloc(&pos, cells * 8) != cudaSuccess || cudaMalloc(&vel, cells * 8) != cudaSuccess ||
+      cudaMalloc(&pb, cells * 8) != cudaSuccess || cudaMalloc(&pbf, h->P.ld * 8) != cudaSuccess ||
+      cudaMalloc(&ctl, sizeof(SpecCtl)) != cudaSuccess || cudaMallocHost(&host, sizeof(SpecCtl)) != cudaSuccess) {
+    for (void* p : {pos, vel, pb, pbf, ctl}) cudaFree(p);
+    if (host) cudaFreeHost(host);
+    cudaGetLastError();
+    return false;  // not enough HBM for two copies: another mode runs
+  }
+  for (void* p : {pos, vel, pb, pbf, ctl}) h->allocs.push_back(p);
+  h->S_alt = KState{static_cast<double*>(pos), static_cast<double*>(vel), static_cast<double*>(pb),
+                    static_cast<double*>(pbf)};
+  h->spec_ctl = static_cast<SpecCtl*>(ctl);
+  h->spec_host = static_cast<SpecCtl*>(host);
+  if (ensure_queue(h, grid) != CUPSO_OK) return false;
+  const char* k = getenv("CUPSO_SPEC_K");
+  h->spec_kmax = k ? std::max(1, atoi(k)) : 64;
+  h->spec_grid = static_cast<int>(grid);
+  return true;
+}
+
+cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
+  SpecCtl& c = *h->spec_host;
+  c = SpecCtl{t0, 1u, 0u, 1u, ~0u, 0u, 0u, 0u};
+  CK(cudaMemcpyAsync(h->spec_ctl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
+  const void* kfn = nullptr;
+  int np = 1;
+  dispatch_fit(h->fid, [&](auto F) { kfn = spec_kernel<decltype(F)::value>(h->P.d, &np); });
+  const uint32_t kmax = h->spec_kmax;
+  KState s0 = h->S, s1 = h->S_alt;
+  void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax)};
+  for (;;) {
+    // passes still needed if no speculation fails from here on
+    uint32_t n = 0, t = c.t0, K = c.K, ks = c.kspec;
+    while (t < t1) {
+      t += K;
+      ++n;
+      if (K >= ks) ks = std::min(2 * ks, kmax);
+      K = std::min(ks, t1 - t);
+    }
+    for (uint32_t i = 0; i < n; ++i)
+      CK(cudaLaunchKernel(kfn, dim3(h->spec_grid), dim3(kSyncThreads), args, 0, h->stream));
+    CK(cudaMemcpyAsync(&c, h->spec_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (c.t0 >= t1) break;
+  }
+  h->spec_passes += c.passes;
+  h->spec_fails += c.fails;
+  if (c.parity) {  // the committed state ended in the second buffer
+    std::swap(h->S, h->S_alt);
+    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+    h->graphs.clear();  // captured graphs hold the old state pointers
+  }
+  return CUPSO_OK;
+}
+
 cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_t t1) {
   if (variant == CUPSO_SYNC && resident_fits(h)) return launch_resident(h, t0, t1);
   if (variant == CUPSO_ASYNC && tiled_fits(h)) return launch_tiled(h, t0, t1);
@@ -647,7 +785,9 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   const uint32_t t0 = h->t, t1 = h->t + iters;
   cudaGraphExec_t ge = nullptr;
   if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
-  const bool wave = variant == CUPSO_SYNC && h->wave && !h->comm;
+  // probe outside the timed region (allocates the second state buffer once)
+  const bool spec = iters && variant == CUPSO_SYNC && !h->comm && spec_fits(h);
+  const bool wave = variant == CUPSO_SYNC && h->wave && !h->comm && !spec;
   if (iters && wave) {
     TRY(wave_graph(h, t0, iters, &ge));
     CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
@@ -657,13 +797,15 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
     TRY(copy_record(h, h->C.live, h->C.snap));
     CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
   }
-  if (iters && variant == CUPSO_SYNC && !wave && !h->comm) resident_fits(h);  // probe outside the timed region
+  if (iters && variant == CUPSO_SYNC && !wave && !spec && !h->comm) resident_fits(h);  // probe outside the timed region
   if (iters && variant == CUPSO_ASYNC) tiled_fits(h);
-  if (iters && ((variant == CUPSO_SYNC && !wave) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
+  if (iters && ((variant == CUPSO_SYNC && !wave && !spec) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
   CK(cudaEventRecord(h->ev0, h->stream));
   if (iters) {
     if (ge) {
       CK(cudaGraphLaunch(ge, h->stream));
+    } else if (spec) {
+      TRY(spec_steps(h, t0, t1));
     } else if (variant == CUPSO_SYNC && h->comm) {
       TRY(sharded_steps(h, t0, t1));
     } else {
@@ -996,6 +1138,7 @@ cupso_status cupso_destroy(cupso_swarm* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
   for (void* p : h->allocs) cudaFree(p);
+  if (h->spec_host) cudaFreeHost(h->spec_host);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -1095,12 +1238,21 @@ size_t cupso_device_bytes(const cupso_swarm* h) {
 
 int cupso_sync_grid_blocks(const cupso_swarm* h) {
   if (!h) return 0;
+  if (h->spec_grid > 0) return h->spec_grid;
   return h->res_grid > 0 ? h->res_grid : h->sync_grid;
+}
+
+cupso_status cupso_spec_stats(const cupso_swarm* h, uint64_t* passes, uint64_t* fails) {
+  if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  if (passes) *passes = h->spec_passes;
+  if (fails) *fails = h->spec_fails;
+  return CUPSO_OK;
 }
 
 int cupso_sync_mode(const cupso_swarm* h) {
   if (!h) return 0;
   if (h->comm) return 4;
+  if (h->spec_grid > 0) return 5;
   if (h->wave) return 2;
   if (h->res_grid > 0) return 3;
   return h->sync_grid > 0 ? 1 : 0;

@@ -510,22 +510,31 @@ struct StepCfg {
   static constexpr int kKD = KD_;  // axes whose loads are issued together (memory-level parallelism)
 };
 
+// NP adjacent particles of one axis row: scalar for NP = 1, 128-bit
+// accesses (NP/2 of them) for even NP; rows are 512-B aligned and units start
+// at multiples of NP, so every access is naturally aligned.
 template <int NP>
 __device__ __forceinline__ void ldv(const double* p, double (&o)[NP]) {
-  if constexpr (NP == 2) {
-    const double2 t = *reinterpret_cast<const double2*>(p);
-    o[0] = t.x;
-    o[1] = t.y;
-  } else {
+  static_assert(NP == 1 || NP % 2 == 0, "NP must be 1 or even");
+  if constexpr (NP == 1) {
     o[0] = *p;
+  } else {
+#pragma unroll
+    for (int k = 0; k < NP; k += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + k);
+      o[k] = t.x;
+      o[k + 1] = t.y;
+    }
   }
 }
 template <int NP>
 __device__ __forceinline__ void stv(double* p, const double (&o)[NP]) {
-  if constexpr (NP == 2) {
-    *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
-  } else {
+  static_assert(NP == 1 || NP % 2 == 0, "NP must be 1 or even");
+  if constexpr (NP == 1) {
     *p = o[0];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NP; k += 2) *reinterpret_cast<double2*>(p + k) = make_double2(o[k], o[k + 1]);
   }
 }
 

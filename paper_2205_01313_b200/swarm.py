@@ -117,10 +117,16 @@ class Swarm:
     def sync_grid_blocks(self) -> int:
         return lib().cupso_sync_grid_blocks(self._h)
 
-    SYNC_MODES = {0: "undecided", 1: "persistent", 2: "wave", 3: "resident", 4: "nccl-sharded"}
+    SYNC_MODES = {0: "undecided", 1: "persistent", 2: "wave", 3: "resident", 4: "nccl-sharded", 5: "spec"}
 
     def sync_mode(self) -> str:
         return self.SYNC_MODES[lib().cupso_sync_mode(self._h)]
+
+    def spec_stats(self) -> tuple[int, int]:
+        """(passes, falsified passes) of the speculative cuda-sync mode on this handle."""
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        check(lib().cupso_spec_stats(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def stream(self) -> int:
         return lib().cupso_stream(self._h) or 0

@@ -1,0 +1,166 @@
+"""GPU parity of the speculative temporally-blocked cuda-sync mode (k_spec).
+
+A pass runs K iterations per particle in registers against a fixed gbest
+snapshot and is re-run exactly when an admission before its last iteration
+falsifies that (paper_2205_01313_b200/csrc/cupso_spec.cuh). The bar is the
+synchronous one (north star): trace, gbest index trajectory, occupancy and the
+full final state bit-identical to run_serial (oracle) / the other synchronous
+engines, for every pass length K and however the iterations are chunked.
+"""
+import numpy as np
+import pytest
+
+from test_gpu_parity import BITWISE_FITNESS, assert_bitwise, assert_close, compare_run
+
+pytestmark = pytest.mark.gpu
+
+FITNESS = ["cubic", "sphere", "rosenbrock", "griewank", "rastrigin"]
+
+
+@pytest.fixture
+def spec_env(monkeypatch):
+    monkeypatch.setenv("CUPSO_SYNC_MODE", "spec")
+    return monkeypatch
+
+
+def run_sync(cupso, fit, n, d, T, seed, chunks=None):
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, seed) as sw:
+        for c in (chunks or [T]):
+            sw.step(cupso.SYNC, c)
+        mode = sw.sync_mode()
+        tr, tp, oc = sw.trace()
+        return dict(mode=mode, trace=tr, trace_particle=tp, occupancy=oc, state=sw.state(), gbest=sw.gbest(),
+                    stats=sw.spec_stats())
+
+
+def compare_state(got, orc, fit, what):
+    for k in ("positions", "velocities", "pbest_pos", "pbest_fit", "fitness"):
+        if fit in BITWISE_FITNESS:
+            assert_bitwise(getattr(got, k), orc.state[k], f"{what} {k}")
+        else:
+            assert_close(getattr(got, k), orc.state[k], f"{what} {k}")
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8])
+@pytest.mark.parametrize("fit", FITNESS)
+def test_spec_matches_oracle(cupso, oracle, spec_env, fit, d):
+    n, T, seed = 3001, 120, 11  # odd n: the last two-particle unit is half padding
+    got = run_sync(cupso, fit, n, d, T, seed)
+    assert got["mode"] == "spec"
+    orc = oracle.run_serial(fit, n, d, T, seed)
+
+    class R:  # compare_run's shape
+        trace, trace_particle = got["trace"], got["trace_particle"]
+        gbest_pos, gbest_particle = got["gbest"].pos, got["gbest"].particle
+    compare_run(R, orc, fit, f"spec {fit} d={d}")
+    compare_state(got["state"], orc, fit, f"spec {fit} d={d}")
+    passes, fails = got["stats"]
+    assert 0 < passes <= T + fails
+
+
+@pytest.mark.parametrize("kmax", ["1", "2", "7", "64"])
+def test_spec_pass_length_invariance(cupso, oracle, spec_env, kmax):
+    spec_env.setenv("CUPSO_SPEC_K", kmax)
+    n, d, T, seed = 5000, 8, 90, 5
+    got = run_sync(cupso, "sphere", n, d, T, seed)
+    orc = oracle.run_serial("sphere", n, d, T, seed)
+    assert_bitwise(got["trace"], orc.trace, f"K={kmax} trace")
+    assert np.array_equal(got["trace_particle"], orc.trace_particle)
+    compare_state(got["state"], orc, "sphere", f"K={kmax}")
+    passes, fails = got["stats"]
+    if kmax == "1":
+        assert fails == 0 and passes == T  # K = 1 passes are exact by construction
+    else:
+        assert passes < T + fails
+
+
+def test_spec_occupancy_matches_queue_engine(cupso, spec_env):
+    """queue_occupancy (admitted / N per iteration) equals the classic queue engine's."""
+    f = cupso.find_fitness("sphere")
+    p = cupso.make_params(f, 4096, 4, 80)
+    occ = {}
+    for v in (cupso.SYNC, cupso.QUEUE):
+        with cupso.Swarm(p, f, 2) as sw:
+            sw.step(v, 80)
+            tr, tp, oc = sw.trace()
+            occ[v] = (tr, tp, oc)
+    assert_bitwise(occ[cupso.SYNC][0], occ[cupso.QUEUE][0], "trace")
+    assert np.array_equal(occ[cupso.SYNC][1], occ[cupso.QUEUE][1])
+    assert_bitwise(occ[cupso.SYNC][2], occ[cupso.QUEUE][2], "occupancy")
+    assert occ[cupso.SYNC][2][0] > 0  # iteration 0 admits particles
+
+
+def test_spec_speculation_is_falsified_and_recovered(cupso, oracle, spec_env):
+    """A swarm whose gbest keeps improving: many passes fail and are re-run, result exact."""
+    n, d, T, seed = 20000, 2, 200, 3
+    got = run_sync(cupso, "rosenbrock", n, d, T, seed)
+    passes, fails = got["stats"]
+    orc = oracle.run_serial("rosenbrock", n, d, T, seed)
+    changes = int(np.count_nonzero(np.diff(orc.trace) != 0))
+    assert changes > 3 and fails > 0, (changes, fails)
+    assert_bitwise(got["trace"], orc.trace, "trace")
+    assert np.array_equal(got["trace_particle"], orc.trace_particle)
+    compare_state(got["state"], orc, "rosenbrock", "recovered")
+
+
+@pytest.mark.parametrize("chunks", [[1] * 12, [5, 7], [3, 1, 8]])
+def test_spec_chunked_steps_and_buffer_swap(cupso, oracle, spec_env, chunks):
+    """Steps of any length compose; the ping-pong buffer swap is invisible to the caller."""
+    n, d, T, seed = 777, 4, 12, 21
+    got = run_sync(cupso, "cubic", n, d, T, seed, chunks=chunks)
+    orc = oracle.run_serial("cubic", n, d, T, seed)
+    assert_bitwise(got["trace"], orc.trace, "trace")
+    compare_state(got["state"], orc, "cubic", f"chunks {chunks}")
+
+
+def test_spec_then_other_variants(cupso, oracle, spec_env):
+    """Variants mixed per step after spec passes (graphs re-captured on the swapped buffers)."""
+    f = cupso.find_fitness("sphere")
+    n, d, T, seed = 1500, 8, 60, 8
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, seed) as sw:
+        for v in [cupso.SYNC, cupso.QUEUE_LOCK, cupso.SYNC, cupso.REDUCTION, cupso.SYNC] * 3 + [cupso.SYNC] * 15:
+            sw.step(v, 3 if v != cupso.SYNC else 2)
+            if sw.iteration >= T:
+                break
+        if sw.iteration < T:
+            sw.step(cupso.SYNC, T - sw.iteration)
+        tr, tp, _ = sw.trace()
+        st = sw.state()
+    orc = oracle.run_serial("sphere", n, d, T, seed)
+    assert_bitwise(tr, orc.trace, "trace")
+    assert np.array_equal(tp, orc.trace_particle)
+    compare_state(st, orc, "sphere", "mixed")
+
+
+def test_spec_single_particle_and_single_iteration(cupso, oracle, spec_env):
+    for n, T in [(1, 40), (2, 1), (3, 17)]:
+        got = run_sync(cupso, "sphere", n, 1, T, 9)
+        orc = oracle.run_serial("sphere", n, 1, T, 9)
+        assert_bitwise(got["trace"], orc.trace, f"n={n} T={T}")
+        compare_state(got["state"], orc, "sphere", f"n={n} T={T}")
+
+
+def test_spec_cfg5_shape_equals_wave(cupso, monkeypatch):
+    """2^22 x d=8 sphere (the cfg5 shape at 1/64 size): spec == wave bitwise, state included."""
+    f = cupso.find_fitness("sphere")
+    n, d, T = 1 << 22, 8, 24
+    p = cupso.make_params(f, n, d, T)
+    out = {}
+    for mode in ("spec", "wave"):
+        monkeypatch.setenv("CUPSO_SYNC_MODE", mode)
+        with cupso.Swarm(p, f, 1) as sw:
+            sw.step(cupso.SYNC, T)
+            assert sw.sync_mode() == mode
+            tr, tp, oc = sw.trace()
+            st = sw.state()
+            out[mode] = (tr, tp, oc, st.positions[::4099].copy(), st.pbest_fit.copy(), sw.spec_stats())
+    a, b = out["spec"], out["wave"]
+    assert_bitwise(a[0], b[0], "trace")
+    assert np.array_equal(a[1], b[1])
+    assert_bitwise(a[2], b[2], "occupancy")
+    assert_bitwise(a[3], b[3], "positions (strided sample)")
+    assert_bitwise(a[4], b[4], "pbest_fit")
+    assert a[5][0] < T  # temporally blocked: fewer passes than iterations
