@@ -171,6 +171,8 @@ struct cupso_swarm {
   SpecCtl* spec_host = nullptr;  // pinned mirror
   uint32_t spec_kmax = 64;
   uint64_t spec_passes = 0, spec_fails = 0;
+  bool areg_checked = false;   // register-resident cuda-async probed
+  int areg_grid = 0, areg_k = 32;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
   std::vector<uint8_t> is_async;
   std::map<std::tuple<int, uint32_t, uint32_t>, cudaGraphExec_t> graphs;
@@ -702,8 +704,63 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   return CUPSO_OK;
 }
 
+// Register-resident mode of cuda-async (k_async_reg): dims 1/2/4/8, each
+// thread runs K iterations on its particles in registers. CUPSO_ASYNC_MODE=
+// reg|tiled|plain selects; CUPSO_ASYNC_K sets K (default 32).
+template <int F, int D>
+const void* async_reg_kernel() {
+  return reinterpret_cast<const void*>(
+      k_async_reg<F, D, SpecKernel<F, D>::kNP, SpecKernel<F, D>::kMinB>);
+}
+template <int F>
+const void* async_reg_kernel(uint32_t d, int* np) {
+  switch (d) {
+    case 1: *np = SpecKernel<F, 1>::kNP; return async_reg_kernel<F, 1>();
+    case 2: *np = SpecKernel<F, 2>::kNP; return async_reg_kernel<F, 2>();
+    case 4: *np = SpecKernel<F, 4>::kNP; return async_reg_kernel<F, 4>();
+    case 8: *np = SpecKernel<F, 8>::kNP; return async_reg_kernel<F, 8>();
+    default: return nullptr;
+  }
+}
+
+bool async_reg_fits(cupso_swarm* h) {
+  if (h->areg_checked) return h->areg_grid > 0;
+  h->areg_checked = true;
+  const char* mode = getenv("CUPSO_ASYNC_MODE");
+  if (mode && strcmp(mode, "reg") != 0 && strcmp(mode, "auto") != 0) return false;
+  const void* kfn = nullptr;
+  int np = 1;
+  dispatch_fit(h->fid, [&](auto F) { kfn = async_reg_kernel<decltype(F)::value>(h->P.d, &np); });
+  if (!kfn) return false;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kSyncThreads, 0) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  const uint64_t units = (h->P.n + np - 1ull) / np;
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
+  const uint64_t rounds = (units + resident - 1) / resident;
+  const uint64_t threads = (units + rounds - 1) / rounds;
+  h->areg_grid = static_cast<int>(std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads));
+  const char* k = getenv("CUPSO_ASYNC_K");
+  h->areg_k = k ? std::max(1, atoi(k)) : 32;
+  return true;
+}
+
+cupso_status launch_async_reg(cupso_swarm* h, uint32_t t0, uint32_t t1) {
+  CK(cudaMemsetAsync(h->C.seq, 0, sizeof(uint32_t), h->stream));
+  const void* kfn = nullptr;
+  int np = 1;
+  dispatch_fit(h->fid, [&](auto F) { kfn = async_reg_kernel<decltype(F)::value>(h->P.d, &np); });
+  uint32_t K = static_cast<uint32_t>(h->areg_k);
+  void* args[] = {&h->P, &h->S, &h->C, &t0, &t1, &K};
+  CK(cudaLaunchKernel(kfn, dim3(h->areg_grid), dim3(kSyncThreads), args, 0, h->stream));
+  return CUPSO_OK;
+}
+
 cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_t t1) {
   if (variant == CUPSO_SYNC && resident_fits(h)) return launch_resident(h, t0, t1);
+  if (variant == CUPSO_ASYNC && async_reg_fits(h)) return launch_async_reg(h, t0, t1);
   if (variant == CUPSO_ASYNC && tiled_fits(h)) return launch_tiled(h, t0, t1);
   TRY(ensure_sync_grid(h));
   const size_t smem = sync_smem(h);
@@ -798,7 +855,7 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
     CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
   }
   if (iters && variant == CUPSO_SYNC && !wave && !spec && !h->comm) resident_fits(h);  // probe outside the timed region
-  if (iters && variant == CUPSO_ASYNC) tiled_fits(h);
+  if (iters && variant == CUPSO_ASYNC && !async_reg_fits(h)) tiled_fits(h);
   if (iters && ((variant == CUPSO_SYNC && !wave && !spec) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
   CK(cudaEventRecord(h->ev0, h->stream));
   if (iters) {

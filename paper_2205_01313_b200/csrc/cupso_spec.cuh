@@ -243,3 +243,228 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
 }
 
 }  // namespace cupso
+
+namespace cupso {
+
+// ------------------------------------------------ async, register-resident
+// The asynchronous variant needs no speculation: a particle may move against
+// whatever gbest was last published, so each thread keeps its particles in
+// registers for K iterations at a time (the temporal blocking of
+// k_async_tiled without SMEM tiles or block barriers). Per warp and unit:
+//   * before the unit's K iterations the warp takes a consistent copy of the
+//     live record (seqlock: even version, unchanged after the copy; skipped
+//     when the version did not move);
+//   * during them the thread only counts admissions (f > its view) into
+//     admitted[t], and an admitted particle becomes the thread's own view of
+//     the gbest (fit and position) -- no polling, no warp collectives in the
+//     iteration loop;
+//   * after them the warp's best pbest that beats the view (beats() order, warp
+//     ballot + shuffle argmax) is published by its lane with the CAS(version
+//     even->odd) protocol of async_commit, and folded into trace_key[t] at the
+//     iteration it was found.
+// Lanes past the end of the swarm run the loop with neutral state so every
+// warp-collective sees all 32 lanes.
+// Out-of-line slow paths of k_async_reg: keeping them out of the iteration
+// loop keeps the loop body inside the instruction cache (inlined, they made
+// the d=1 loop ~7x slower with no call ever taken after warm-up).
+//
+// Warp-collective: copy a consistent (even, unchanged) version of the live
+// record into the warp's SMEM slot; returns the version read.
+__device__ __noinline__ uint32_t areg_refresh(const KCtl& C, uint32_t d, uint32_t gver, double* slot,
+                                             uint64_t ts) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (;;) {
+    uint32_t v = 0;
+    if (lane == 0) v = ld_acquire_gpu(C.seq);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    if (v & 1u) {  // a writer holds the record: back off instead of hammering its L2 line
+      if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+      __nanosleep(200);
+      continue;
+    }
+    if (v == gver) return v;
+    __syncwarp();
+    if (lane == 0) slot[0] = __ldcg(&C.live->fit);
+    for (uint32_t a = lane; a < d; a += 32) slot[1 + a] = __ldcg(&C.live_pos[a]);
+    __threadfence();
+    uint32_t v2 = 0;
+    if (lane == 0) v2 = ld_acquire_gpu(C.seq);
+    v2 = __shfl_sync(0xffffffffu, v2, 0);
+    __syncwarp();
+    if (v2 == v) return v;
+  }
+}
+
+// One lane: publish (wf, wi, pos[0..d)) into the live record if it still
+// beats it (lock-free pre-check, CAS(version even->odd), re-check, write,
+// release version+2). Returns the best fitness this lane knows afterwards.
+__device__ __noinline__ double areg_publish(const KCtl& C, uint32_t d, double wf, uint32_t wi, const double* pos,
+                                            double view) {
+  const double lf0 = ld_acquire_gpu_f64(&C.live->fit);
+  view = lf0 > view ? lf0 : view;
+  if (!may_beat(C.live, wf, wi)) return view;
+  const uint64_t tl = globaltimer_ns();
+  uint32_t sv;
+  for (;;) {
+    sv = ld_acquire_gpu(C.seq);
+    if (!(sv & 1u) && atomicCAS(C.seq, sv, sv + 1u) == sv) break;
+    // lost the race: give up as soon as the record no longer loses to us
+    // (after warm-up thousands of warps publish at once; re-checking turns
+    // their CAS storm on one L2 line into reads)
+    if (!may_beat(C.live, wf, wi)) return view;
+    if (globaltimer_ns() - tl > kSpinTimeoutNs) __trap();
+    __nanosleep(100);
+  }
+  __threadfence();
+  const double lf = __ldcg(&C.live->fit);
+  const uint32_t lp = __ldcg(&C.live->particle);
+  if (beats(wf, wi, lf, lp)) {
+    for (uint32_t a = 0; a < d; ++a) C.live_pos[a] = pos[a];
+    write_rec(C.live, wf, wi);
+    view = wf;
+  } else {
+    view = lf > view ? lf : view;
+  }
+  __threadfence();
+  st_release_gpu(C.seq, sv + 2u);
+  return view;
+}
+
+template <int F, int D, int NP, int MINB>
+__global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KState S, KCtl C, uint32_t t0,
+                                                                 uint32_t t1, uint32_t K) {
+  __shared__ double s_slot[kSyncWarps][1 + D];  // per warp: copy of the live record
+  __shared__ double s_pub[kSyncWarps][D];       // per warp: the publisher's position
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* slot = s_slot[warp];
+  const uint64_t ts = globaltimer_ns();
+  double gp[D];
+  double gfit;
+  uint32_t gver = 0xffffffffu;
+  const uint32_t units = (P.n + NP - 1) / NP;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t wbase = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  const size_t ld = P.ld;
+  for (uint32_t tb = t0; tb < t1; tb += K) {
+    const uint32_t te = min(tb + K, t1);
+    for (uint32_t u0 = wbase; u0 < units; u0 += stride) {  // warp-uniform trip count
+      // the latest published gbest for this unit's K iterations
+      gver = areg_refresh(C, D, gver, slot, ts);
+      gfit = slot[0];
+#pragma unroll
+      for (int a = 0; a < D; ++a) gp[a] = slot[1 + a];
+      const uint32_t u = u0 + lane;
+      const bool live = u < units;
+      const uint32_t li = NP * u, g0 = P.base + li;
+      double x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
+      bool ok[NP];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) ok[k] = live && (k == 0 || li + k < P.n);
+      if (live) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const size_t at = static_cast<size_t>(a) * ld + li;
+          ldv<NP>(S.pos + at, x[a]);
+          ldv<NP>(S.vel + at, v[a]);
+          ldv<NP>(S.pb + at, pb[a]);
+        }
+        ldv<NP>(S.pbf + li, pbf);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          pbf[k] = -INFINITY;
+#pragma unroll
+          for (int a = 0; a < D; ++a) x[a][k] = v[a][k] = pb[a][k] = 0.0;
+        }
+      }
+      bool dirty = false;
+      uint32_t tfound = 0;  // iteration of this thread's latest admission
+      for (uint32_t t = tb; t < te; ++t) {
+        Fit<F> acc[NP];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            const double r1 = uniform01(P, t, g0 + k, a, 0);
+            const double r2 = uniform01(P, t, g0 + k, a, 1);
+            v[a][k] = vel_step(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
+            x[a][k] = pos_step(P, x[a][k], v[a][k]);
+            acc[k].add(x[a][k], a);
+          }
+        }
+        uint32_t adm = 0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const double f = acc[k].value();
+          if (!ok[k]) continue;
+          if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
+            dirty = true;
+            pbf[k] = f;
+#pragma unroll
+            for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+          }
+          if (f > gfit) {  // beats this thread's view of the gbest: it becomes the view
+            ++adm;
+            gfit = f;
+#pragma unroll
+            for (int a = 0; a < D; ++a) gp[a] = x[a][k];
+          }
+        }
+        if (adm) {  // rare after warm-up; one atomic per warp
+          const unsigned m = __activemask();
+          const uint32_t wadm = __reduce_add_sync(m, adm);
+          if (lane == static_cast<uint32_t>(__ffs(m) - 1))
+            atomicAdd(&C.admitted[t], static_cast<unsigned long long>(wadm));
+          tfound = t;
+        }
+      }
+      // Publish: the unit's pbests that beat the view are gbest candidates
+      // (the gbest is the max of all pbests); the warp's best in beats()
+      // order goes to the live record once per unit instead of per iteration.
+      double bf = -INFINITY;
+      uint32_t bi = kNoParticle, bk = 0;
+      const double view = slot[0];  // the unit's starting view (gfit may hold own finds)
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (ok[k] && pbf[k] > view && beats(pbf[k], g0 + k, bf, bi)) {
+          bf = pbf[k];
+          bi = g0 + k;
+          bk = k;
+        }
+      if (__any_sync(0xffffffffu, bi != kNoParticle)) {
+        double wf = bf;
+        uint32_t wi = bi;
+        warp_argmax(wf, wi);
+        __syncwarp();
+        if (bi == wi && bi != kNoParticle) {  // the winning lane publishes
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            double pa = pb[a][0];
+#pragma unroll
+            for (int k = 1; k < NP; ++k)
+              if (bk == static_cast<uint32_t>(k)) pa = pb[a][k];
+            s_pub[warp][a] = pa;
+          }
+          const double seen = areg_publish(C, D, wf, wi, s_pub[warp], view);
+          atomicMax(&C.trace_key[tfound], order_key(seen));
+        }
+        __syncwarp();
+      }
+      if (live) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const size_t at = static_cast<size_t>(a) * ld + li;
+          stv<NP>(S.pos + at, x[a]);
+          stv<NP>(S.vel + at, v[a]);
+        }
+        if (dirty) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) stv<NP>(S.pb + static_cast<size_t>(a) * ld + li, pb[a]);
+          stv<NP>(S.pbf + li, pbf);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace cupso

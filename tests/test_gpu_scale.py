@@ -114,6 +114,11 @@ def test_variants_can_be_mixed_per_iteration(cupso, oracle):
 
 
 # ------------------------------------------------------------------- async
+def sw_initial(cupso, p, f, seed):
+    with cupso.Swarm(p, f, seed) as sw:
+        return sw.initial_gbest()[0]
+
+
 def test_async_statistics_32_seeds(cupso):
     """North star: the asynchronous variant is checked statistically, final
     fitness over 32 seeds against the synchronous variant."""
@@ -129,20 +134,21 @@ def test_async_statistics_32_seeds(cupso):
     assert np.median(-asy) < 1.0
 
 
-@pytest.mark.parametrize("mode", ["plain", "tiled"])
-def test_async_invariants(cupso, oracle, monkeypatch, mode):
-    """Both async schedules (free-running blocks; SMEM tiles advanced K iterations
-    at a time) keep a consistent, monotone global best."""
+@pytest.mark.parametrize("mode,d", [("plain", 3), ("tiled", 3), ("reg", 1), ("reg", 4), ("reg", 8)])
+def test_async_invariants(cupso, oracle, monkeypatch, mode, d):
+    """Every async schedule (free-running blocks; SMEM tiles or registers
+    advanced K iterations at a time) keeps a consistent, monotone global best."""
     monkeypatch.setenv("CUPSO_ASYNC_MODE", mode)
     monkeypatch.setenv("CUPSO_ASYNC_K", "5")
     f = cupso.find_fitness("cubic")
-    p = cupso.make_params(f, 100000, 3, 80)
+    p = cupso.make_params(f, 100001, d, 80)
     with cupso.Swarm(p, f, 2) as sw:
         sw.step(cupso.ASYNC, 80)
         tr, _, occ = sw.trace()
         gb = sw.gbest()
         st = sw.state()
-    assert (np.diff(tr) >= 0).all()
+    assert (np.diff(tr) >= 0).all() and tr[0] >= sw_initial(cupso, p, f, 2)
+    assert np.isfinite(st.positions).all() and (np.abs(st.positions) <= f.hi).all()
     assert tr[-1] == gb.fit
     assert oracle.fitness("cubic", gb.pos) == gb.fit  # the record is a consistent (fit, pos) pair
     assert gb.fit == st.pbest_fit.max()
