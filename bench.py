@@ -141,9 +141,13 @@ def ncu_entry(workload: str, variant: str) -> dict:
 
 
 def ncu_traffic(workload: str, variant: str):
-    """dram bytes per launch from the committed ncu summary, or None."""
+    """(dram bytes per iteration, 1) from the committed ncu summary, or (None, None)."""
     e = ncu_entry(workload, variant)
-    return (e["dram_bytes_per_launch"], e.get("iters_per_launch")) if e else (None, None)
+    if not e:
+        return None, None
+    if e.get("dram_bytes_per_iter") is not None:
+        return e["dram_bytes_per_iter"], 1
+    return e["dram_bytes_per_launch"], e.get("iters_per_launch")
 
 
 def cpu_reference_leg(fitness, n, d, max_seconds=12.0, sample_iters=None):
@@ -219,7 +223,7 @@ def run_reference_arm(args, world, rank):
     line = {
         "impl": "reference", "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * secs / len(vals), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * secs / len(vals), "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox init of the reference)",
         "config": {"workload": desc, "fitness": fitness, "particles": n_rank, "dims": d,
                    "iterations_per_step": iters, "engine": "reference queue-lock (all host threads)"},
@@ -300,6 +304,7 @@ def main():
         barrier()
         sw.step(engine.variant, T)
     per_step = []
+    spec0 = sw.spec_stats()
     barrier()
     with ClockSampler(local) as clk:
         for k in range(args.steps):
@@ -321,13 +326,23 @@ def main():
 
     # ---- roofline of the dominant kernel (one launch = T iterations for the persistent kernels) ----
     bytes_per_pu = (5 * d + 1) * 8
-    # cuda-sync runs persistent (1 cooperative launch per step; grid > 0) or as
-    # a graph of one wave per iteration (grid == 0); shards: propose+commit per iteration
-    persistent = variant_name == "cuda-async" or (variant_name == "cuda-sync" and world == 1 and grid > 0)
-    launches_per_step = {"cuda-sync": 1 if persistent else (2 * T if world > 1 else T), "cuda-async": 1,
+    # cuda-sync runs as speculative passes (k_spec: ~T/K launches per step),
+    # persistent (1 cooperative launch per step) or as a graph of one wave per
+    # iteration; shards: propose+commit per iteration
+    mode = sw.sync_mode() if variant_name == "cuda-sync" else None
+    amode = sw.async_mode() if variant_name == "cuda-async" else None
+    spec1 = sw.spec_stats()
+    spec_passes = (spec1[0] - spec0[0]) / K
+    spec_launches = (spec1[2] - spec0[2]) / K
+    spec = mode in ("spec", "nccl-sharded-spec")
+    persistent = variant_name == "cuda-async" or (variant_name == "cuda-sync" and world == 1 and grid > 0
+                                                  and not spec)
+    # sharded spec: k_spec + k_spec_commit per pass (the all-gather is NCCL's)
+    launches_per_step = {"cuda-sync": (spec_launches * (2 if world > 1 else 1)) if spec else
+                         (1 if persistent else (2 * T if world > 1 else T)), "cuda-async": 1,
                          "cuda-queue-lock": T, "cuda-queue": 2 * T, "cuda-reduction": 2 * T,
                          "cuda-unrolled": 2 * T}[variant_name]
-    iters_per_launch = T if persistent else 1
+    iters_per_launch = T if persistent else (T / spec_passes if spec else 1)
     launch_secs = (dev_secs / K) / (T / iters_per_launch)
     alg_bytes = count * iters_per_launch * bytes_per_pu
     peak, peak_src = measured_peak_gbs()
@@ -335,18 +350,26 @@ def main():
     traffic, traffic_iters = ncu_traffic(args.workload, variant_name)
     if traffic is not None and traffic_iters:
         traffic = traffic * iters_per_launch / traffic_iters
-    mode = sw.sync_mode() if variant_name == "cuda-sync" else None
     sync_kernel = {"resident": f"k_sync_res<{fitness},{d if d == 1 else 0}>", "persistent": f"k_sync<{fitness}>",
-                   "wave": f"k_wave<{fitness}>"}.get(mode, f"k_propose<{fitness}>+k_commit")
+                   "wave": f"k_wave<{fitness}>", "spec": f"k_spec<{fitness},{d}>",
+                   "nccl-sharded-spec": f"k_spec<{fitness},{d}>+k_spec_commit"}.get(
+                       mode, f"k_propose<{fitness}>+k_commit")
+    async_kernel = {"reg": f"k_async_reg<{fitness},{d}>", "tiled": f"k_async_tiled<{fitness}>"}.get(
+        amode, f"k_async<{fitness}>")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
                 "kernel": {"cuda-sync": sync_kernel,
-                           "cuda-async": f"k_async<{fitness}>"}.get(variant_name, f"k_classic_step<{fitness}>"),
+                           "cuda-async": async_kernel}.get(variant_name, f"k_classic_step<{fitness}>"),
+                "mode": mode or amode,
                 "traffic_note": "ncu dram read+write per launch (profiles/ncu_summary_r01.json); "
                                 "below alg bytes = L2-resident state, above = pbest write-backs",
                 "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
                 "bytes_per_particle_update": bytes_per_pu}
-    if mode == "resident":
+    if spec:
+        roofline["spec"] = {"passes_per_step": spec_passes, "launches_per_step": spec_launches,
+                            "falsified_per_step": (spec1[1] - spec0[1]) / K,
+                            "iters_per_pass": T / spec_passes if spec_passes else None}
+    if mode in ("resident", "spec", "nccl-sharded-spec") or amode == "reg":
         # The swarm lives in SMEM for the whole launch: HBM carries ~0 bytes per
         # iteration, so the algorithmic-bytes figure above can exceed
         # the HBM roof. The binding roof is instruction issue (Philox IMAD/LOP3 +
@@ -354,7 +377,7 @@ def main():
         # capture vs 148 SMs x 4 schedulers x SM clock.
         e = ncu_entry(args.workload, variant_name)
         if e.get("warp_inst_per_launch"):
-            winst_iter = e["warp_inst_per_launch"] / e["iters_per_launch"]
+            winst_iter = e.get("warp_inst_per_iter") or e["warp_inst_per_launch"] / e["iters_per_launch"]
             sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
             nsm = torch.cuda.get_device_properties(dev).multi_processor_count
             ach = winst_iter * T * K / dev_secs
@@ -363,8 +386,13 @@ def main():
                 "unit": "G warp-instructions/s", "frac": ach / (nsm * 4 * sm_hz),
                 "inst_per_particle_update": winst_iter * 32 / count,
                 "source": "smsp__inst_executed.sum of " + e.get("capture", "?")}
-        roofline["note"] = ("SMEM-resident swarm (k_sync_res): state read/written once per launch, not per "
-                            "iteration; frac > 1 means the HBM model does not bind -- see issue_roofline")
+        roofline["note"] = {
+            "resident": "SMEM-resident swarm (k_sync_res): state read/written once per launch, not per iteration",
+            "spec": "temporally blocked (k_spec): each pass reads/writes the state once for K iterations held in "
+                    "registers",
+            "nccl-sharded-spec": "temporally blocked shards (k_spec): one all-gather of a pass record per pass",
+        }.get(mode, "temporally blocked (k_async_reg): state read/written once per K iterations held in registers") \
+            + "; frac > 1 means the HBM model does not bind -- see issue_roofline"
 
     extra = {}
     # ---- the in-repo reduction baseline kernel on the same workload (rank 0, N=1) ----
@@ -385,6 +413,7 @@ def main():
     # ---- e2e through the reference-facing C-ABI call (cupso_run), host buffers ----
     e2e = None
     if world == 1:
+        sw.close()  # cupso_run owns its own device swarm (cfg5: 2 x 52 GB double-buffered)
         e2e_secs = []
         for k in range(1 + args.steps):
             torch.cuda.synchronize()
@@ -429,7 +458,7 @@ def main():
         line = {
             "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
             "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * dev_secs / K,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Philox-initialised swarm, reference make_params defaults)",
             "config": {"workload": desc, "fitness": fitness, "particles_total": n_total,
                        "particles_per_gpu": count, "dims": d, "iterations_per_step": T,

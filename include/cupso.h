@@ -151,13 +151,19 @@ size_t cupso_device_bytes(const cupso_swarm* h);
 int cupso_sync_grid_blocks(const cupso_swarm* h);    /* persistent grid size (after a SYNC step) */
 /* How cuda-sync runs on this handle: 0 not yet decided, 1 persistent
  * (k_sync), 2 graph of waves (k_wave), 3 SMEM-resident persistent
- * (k_sync_res), 4 NCCL-sharded (k_propose/k_commit), 5 speculative
- * temporally-blocked passes (k_spec; dims 1/2/4/8). */
+ * (k_sync_res), 4 NCCL-sharded per iteration (k_propose/k_commit), 5
+ * speculative temporally-blocked passes (k_spec / k_spec_split; dims
+ * 1/2/4/8/16/32/64), 6 NCCL-sharded speculative passes (k_spec + one
+ * all-gather of a SpecRec per pass + k_spec_commit). */
 int cupso_sync_mode(const cupso_swarm* h);
-/* Speculative mode bookkeeping since the handle was created: passes launched
- * that did work, and how many of them were falsified by an early admission
- * (each such pass is followed by an exact re-run). */
-cupso_status cupso_spec_stats(const cupso_swarm* h, uint64_t* passes, uint64_t* fails);
+/* Speculative mode bookkeeping since the handle was created: passes that did
+ * work, how many of them were falsified by an early admission (each such pass
+ * is followed by an exact re-run), and kernel launches issued (passes plus the
+ * no-op launches left over when the host's estimate overshoots). */
+cupso_status cupso_spec_stats(const cupso_swarm* h, uint64_t* passes, uint64_t* fails, uint64_t* launches);
+/* How cuda-async runs on this handle: 0 not yet decided, 1 free-running
+ * blocks (k_async), 2 SMEM tiles (k_async_tiled), 3 registers (k_async_reg). */
+int cupso_async_mode(const cupso_swarm* h);
 
 /* ---- multi-GPU shard exchange (one exchange step per iteration) ----
  * A candidate record is cupso_record_bytes(dims) bytes:

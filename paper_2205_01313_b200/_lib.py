@@ -89,7 +89,8 @@ SIGNATURES = {
     "cupso_device_bytes": (C.c_size_t, [_vp]),
     "cupso_sync_grid_blocks": (C.c_int, [_vp]),
     "cupso_sync_mode": (C.c_int, [_vp]),
-    "cupso_spec_stats": (C.c_int, [_vp, _vp, _vp]),
+    "cupso_spec_stats": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "cupso_async_mode": (C.c_int, [_vp]),
     "cupso_record_bytes": (C.c_size_t, [C.c_uint32]),
     "cupso_shard_snapshot": (C.c_int, [_vp, _vp]),
     "cupso_shard_adopt": (C.c_int, [_vp, _vp, C.c_uint32]),

@@ -170,7 +170,10 @@ struct cupso_swarm {
   SpecCtl* spec_ctl = nullptr; // device pass schedule
   SpecCtl* spec_host = nullptr;  // pinned mirror
   uint32_t spec_kmax = 64;
-  uint64_t spec_passes = 0, spec_fails = 0;
+  size_t spec_smem = 0;        // dynamic SMEM of the chosen spec kernel
+  unsigned char* spec_rec_local = nullptr;  // this shard's SpecRec of the running pass
+  unsigned char* spec_rec_all = nullptr;    // [nranks] all-gathered records (sharded)
+  uint64_t spec_passes = 0, spec_fails = 0, spec_launches = 0;
   bool areg_checked = false;   // register-resident cuda-async probed
   int areg_grid = 0, areg_k = 32;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
@@ -589,58 +592,105 @@ struct SpecKernel {
   static const void* fn() { return reinterpret_cast<const void*>(k_spec<F, D, kNP, kMinB>); }
 };
 
-// Alternative (NP, MINB) tunings for the BASELINE dims, selected with
-// CUPSO_SPEC_CFG=<n> (exploration; 0 = the default above).
-template <int F>
-const void* spec_kernel_alt(uint32_t d, int cfg, int* np) {
-  if (d == 1) {
-    switch (cfg) {
-      case 1: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 1, 1, 4>);
-      case 2: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 1, 1, 6>);
-      case 3: *np = 2; return reinterpret_cast<const void*>(k_spec<F, 1, 2, 4>);
-      case 5: *np = 4; return reinterpret_cast<const void*>(k_spec<F, 1, 4, 3>);
-      case 6: *np = 8; return reinterpret_cast<const void*>(k_spec<F, 1, 8, 1>);
-      case 4: *np = 2; return reinterpret_cast<const void*>(k_spec<F, 1, 2, 6>);
-    }
-  } else if (d == 8) {
-    switch (cfg) {
-      case 1: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 8, 1, 3>);
-      case 2: *np = 1; return reinterpret_cast<const void*>(k_spec<F, 8, 1, 1>);
-    }
-  }
-  return nullptr;
+// The speculative kernel chosen for a swarm: function, particles per thread
+// unit, lanes per particle, dynamic SMEM bytes (SMEM-resident lane state).
+struct SpecPick {
+  const void* fn = nullptr;
+  int np = 1, g = 1;
+  size_t smem = 0;
+};
+
+template <int F, int DL, int G, int MINB, bool SM>
+SpecPick split_pick() {
+  SpecPick k;
+  k.fn = reinterpret_cast<const void*>(k_spec_split<F, DL, G, MINB, SM>);
+  k.g = G;
+  constexpr size_t tw = (sizeof(typename Fit<F>::Term) + 7) / 8;
+  k.smem = SM ? (3ull + (sizeof(typename Fit<F>::Term) >= 8 ? tw : 0)) * DL * kSyncThreads * sizeof(double) : 0;
+  return k;
+}
+template <int F, int NP, int MINB>
+SpecPick d1_pick() {
+  SpecPick k;
+  k.fn = reinterpret_cast<const void*>(k_spec<F, 1, NP, MINB>);
+  k.np = NP;
+  return k;
 }
 
+// Alternative tunings for the BASELINE dims, selected with CUPSO_SPEC_CFG=<n>
+// (exploration; 0 = the default).
 template <int F>
-const void* spec_kernel(uint32_t d, int* np) {
-  if (const char* e = getenv("CUPSO_SPEC_CFG"))
-    if (const void* k = spec_kernel_alt<F>(d, atoi(e), np)) return k;
-  switch (d) {
-    case 1: *np = SpecKernel<F, 1>::kNP; return SpecKernel<F, 1>::fn();
-    case 2: *np = SpecKernel<F, 2>::kNP; return SpecKernel<F, 2>::fn();
-    case 4: *np = SpecKernel<F, 4>::kNP; return SpecKernel<F, 4>::fn();
-    case 8: *np = SpecKernel<F, 8>::kNP; return SpecKernel<F, 8>::fn();
-    default: return nullptr;
+SpecPick spec_kernel_alt(uint32_t d, int cfg) {
+  if (d == 32) {
+    switch (cfg) {
+      case 1: return split_pick<F, 4, 8, 2, false>();
+      case 2: return split_pick<F, 8, 4, 1, false>();
+      case 3: return split_pick<F, 4, 8, 3, false>();
+      case 4: return split_pick<F, 8, 4, 3, true>();
+      case 5: return split_pick<F, 8, 4, 4, true>();
+      case 6: return split_pick<F, 4, 8, 4, true>();
+      case 7: return split_pick<F, 8, 4, 2, true>();
+    }
   }
+  if (d == 1) {
+    switch (cfg) {
+      case 1: return d1_pick<F, 1, 4>();
+      case 2: return d1_pick<F, 1, 6>();
+      case 3: return d1_pick<F, 2, 4>();
+      case 5: return d1_pick<F, 4, 3>();
+      case 6: return d1_pick<F, 8, 1>();
+    }
+  } else if (d == 8) {
+    SpecPick k;
+    switch (cfg) {
+      case 1: k.fn = reinterpret_cast<const void*>(k_spec<F, 8, 1, 3>); return k;
+      case 2: k.fn = reinterpret_cast<const void*>(k_spec<F, 8, 1, 1>); return k;
+    }
+  }
+  return {};
+}
+
+// The speculative kernel for dims d ({} when d has no instantiation): whole
+// particle per thread in registers for d <= 8, G lanes x 8 axes beyond.
+template <int F>
+SpecPick spec_kernel(uint32_t d) {
+  if (const char* e = getenv("CUPSO_SPEC_CFG")) {
+    const SpecPick k = spec_kernel_alt<F>(d, atoi(e));
+    if (k.fn) return k;
+  }
+  SpecPick k;
+  switch (d) {
+    case 1: k.np = SpecKernel<F, 1>::kNP; k.fn = SpecKernel<F, 1>::fn(); break;
+    case 2: k.np = SpecKernel<F, 2>::kNP; k.fn = SpecKernel<F, 2>::fn(); break;
+    case 4: k.np = SpecKernel<F, 4>::kNP; k.fn = SpecKernel<F, 4>::fn(); break;
+    case 8: k.np = SpecKernel<F, 8>::kNP; k.fn = SpecKernel<F, 8>::fn(); break;
+    case 16: return split_pick<F, 8, 2, 2, false>();
+    case 32: return split_pick<F, 8, 4, 2, false>();
+    case 64: return split_pick<F, 8, 8, 2, false>();
+  }
+  return k;
 }
 
 bool spec_fits(cupso_swarm* h) {
   if (h->spec_checked) return h->spec_grid > 0;
   h->spec_checked = true;
-  if (h->comm) return false;
   if (const char* e = getenv("CUPSO_SYNC_MODE"))
     if (strcmp(e, "spec") != 0 && strcmp(e, "auto") != 0) return false;
-  const void* kfn = nullptr;
-  int np = 1;
-  dispatch_fit(h->fid, [&](auto F) { kfn = spec_kernel<decltype(F)::value>(h->P.d, &np); });
-  if (!kfn) return false;
+  SpecPick k;
+  dispatch_fit(h->fid, [&](auto F) { k = spec_kernel<decltype(F)::value>(h->P.d); });
+  if (!k.fn) return false;
+  const int np = k.np, g = k.g;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kSyncThreads, 0) != cudaSuccess || per_sm < 1) {
+  if ((k.smem && cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(k.smem)) != cudaSuccess) ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kSyncThreads, k.smem) != cudaSuccess ||
+      per_sm < 1) {
     cudaGetLastError();
     return false;
   }
-  // balanced grid: every thread takes the same number of units
-  const uint64_t units = (h->P.n + np - 1ull) / np;
+  h->spec_smem = k.smem;
+  // balanced grid: every thread takes the same number of units (g lanes per unit)
+  const uint64_t units = (h->P.n + np - 1ull) / np * g;
   const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
   const uint64_t rounds = (units + resident - 1) / resident;
   const uint64_t threads = (units + rounds - 1) / rounds;
@@ -648,22 +698,28 @@ bool spec_fits(cupso_swarm* h) {
   // second state buffer (the pass writes B while A stays intact for a re-run)
   const size_t cells = h->P.ld * h->P.d;
   void *pos = nullptr, *vel = nullptr, *pb = nullptr, *pbf = nullptr, *ctl = nullptr, *host = nullptr;
+  void *rl = nullptr, *ra = nullptr;
+  const size_t rb = spec_rec_bytes(h->P.d);
   if (cudaMalloc(&pos, cells * 8) != cudaSuccess || cudaMalloc(&vel, cells * 8) != cudaSuccess ||
       cudaMalloc(&pb, cells * 8) != cudaSuccess || cudaMalloc(&pbf, h->P.ld * 8) != cudaSuccess ||
-      cudaMalloc(&ctl, sizeof(SpecCtl)) != cudaSuccess || cudaMallocHost(&host, sizeof(SpecCtl)) != cudaSuccess) {
-    for (void* p : {pos, vel, pb, pbf, ctl}) cudaFree(p);
+      cudaMalloc(&ctl, sizeof(SpecCtl)) != cudaSuccess || cudaMalloc(&rl, rb) != cudaSuccess ||
+      cudaMalloc(&ra, rb * std::max(1, h->nranks)) != cudaSuccess ||
+      cudaMallocHost(&host, sizeof(SpecCtl)) != cudaSuccess) {
+    for (void* p : {pos, vel, pb, pbf, ctl, rl, ra}) cudaFree(p);
     if (host) cudaFreeHost(host);
     cudaGetLastError();
     return false;  // not enough HBM for two copies: another mode runs
   }
-  for (void* p : {pos, vel, pb, pbf, ctl}) h->allocs.push_back(p);
+  for (void* p : {pos, vel, pb, pbf, ctl, rl, ra}) h->allocs.push_back(p);
+  h->spec_rec_local = static_cast<unsigned char*>(rl);
+  h->spec_rec_all = static_cast<unsigned char*>(ra);
   h->S_alt = KState{static_cast<double*>(pos), static_cast<double*>(vel), static_cast<double*>(pb),
                     static_cast<double*>(pbf)};
   h->spec_ctl = static_cast<SpecCtl*>(ctl);
   h->spec_host = static_cast<SpecCtl*>(host);
   if (ensure_queue(h, grid) != CUPSO_OK) return false;
-  const char* k = getenv("CUPSO_SPEC_K");
-  h->spec_kmax = k ? std::max(1, atoi(k)) : 64;
+  const char* ke = getenv("CUPSO_SPEC_K");
+  h->spec_kmax = ke ? std::max(1, atoi(ke)) : 64;
   h->spec_grid = static_cast<int>(grid);
   return true;
 }
@@ -673,12 +729,15 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   c = SpecCtl{t0, 1u, 0u, 1u, ~0u, 0u, 0u, 0u};
   CK(cudaMemcpyAsync(h->spec_ctl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
-  const void* kfn = nullptr;
-  int np = 1;
-  dispatch_fit(h->fid, [&](auto F) { kfn = spec_kernel<decltype(F)::value>(h->P.d, &np); });
+  SpecPick k;
+  dispatch_fit(h->fid, [&](auto F) { k = spec_kernel<decltype(F)::value>(h->P.d); });
+  const void* kfn = k.fn;
   const uint32_t kmax = h->spec_kmax;
   KState s0 = h->S, s1 = h->S_alt;
-  void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax)};
+  int sharded = h->comm != nullptr;
+  unsigned char* rec = h->spec_rec_local;
+  void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec, &sharded};
+  const size_t rb = spec_rec_bytes(h->P.d);
   for (;;) {
     // passes still needed if no speculation fails from here on
     uint32_t n = 0, t = c.t0, K = c.K, ks = c.kspec;
@@ -688,8 +747,19 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
       if (K >= ks) ks = std::min(2 * ks, kmax);
       K = std::min(ks, t1 - t);
     }
-    for (uint32_t i = 0; i < n; ++i)
-      CK(cudaLaunchKernel(kfn, dim3(h->spec_grid), dim3(kSyncThreads), args, 0, h->stream));
+    for (uint32_t i = 0; i < n; ++i) {
+      CK(cudaLaunchKernel(kfn, dim3(h->spec_grid), dim3(kSyncThreads), args, h->spec_smem, h->stream));
+      if (sharded) {  // one exchange per pass: the shards' records, then the same decision everywhere
+        const int r = nccl().allGather(h->spec_rec_local, h->spec_rec_all, rb, /*ncclInt8*/ 0, h->comm, h->stream);
+        if (r != 0)
+          return fail(CUPSO_ERUNTIME, "ncclAllGather (spec pass) failed: %s",
+                      nccl().getErrorString ? nccl().getErrorString(r) : "?");
+        k_spec_commit<<<1, 256, 0, h->stream>>>(h->P, h->C, h->spec_ctl, h->spec_rec_all,
+                                                 static_cast<uint32_t>(h->nranks), t1, kmax);
+        CK(cudaGetLastError());
+      }
+    }
+    h->spec_launches += n;
     CK(cudaMemcpyAsync(&c, h->spec_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (c.t0 >= t1) break;
@@ -843,7 +913,7 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   cudaGraphExec_t ge = nullptr;
   if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
   // probe outside the timed region (allocates the second state buffer once)
-  const bool spec = iters && variant == CUPSO_SYNC && !h->comm && spec_fits(h);
+  const bool spec = iters && variant == CUPSO_SYNC && spec_fits(h);
   const bool wave = variant == CUPSO_SYNC && h->wave && !h->comm && !spec;
   if (iters && wave) {
     TRY(wave_graph(h, t0, iters, &ge));
@@ -1299,16 +1369,24 @@ int cupso_sync_grid_blocks(const cupso_swarm* h) {
   return h->res_grid > 0 ? h->res_grid : h->sync_grid;
 }
 
-cupso_status cupso_spec_stats(const cupso_swarm* h, uint64_t* passes, uint64_t* fails) {
+int cupso_async_mode(const cupso_swarm* h) {
+  if (!h) return 0;
+  if (h->areg_grid > 0) return 3;
+  if (h->tile_cap > 0) return 2;
+  return h->sync_grid > 0 ? 1 : 0;
+}
+
+cupso_status cupso_spec_stats(const cupso_swarm* h, uint64_t* passes, uint64_t* fails, uint64_t* launches) {
   if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
   if (passes) *passes = h->spec_passes;
   if (fails) *fails = h->spec_fails;
+  if (launches) *launches = h->spec_launches;
   return CUPSO_OK;
 }
 
 int cupso_sync_mode(const cupso_swarm* h) {
   if (!h) return 0;
-  if (h->comm) return 4;
+  if (h->comm) return h->spec_grid > 0 ? 6 : 4;
   if (h->spec_grid > 0) return 5;
   if (h->wave) return 2;
   if (h->res_grid > 0) return 3;
@@ -1409,6 +1487,11 @@ cupso_status cupso_nccl_init(cupso_swarm* h, const void* unique_id, int nranks, 
   h->rec_all = static_cast<unsigned char*>(all);
   h->comm = comm;
   h->nranks = nranks;
+  if (h->spec_rec_all) {  // spec buffers set up before the exchange existed: size them for nranks
+    void* ra = nullptr;
+    TRY(dmalloc(h, &ra, spec_rec_bytes(h->P.d) * nranks));
+    h->spec_rec_all = static_cast<unsigned char*>(ra);
+  }
   h->rank = rank;
   return CUPSO_OK;
 }

@@ -92,34 +92,63 @@ __device__ __forceinline__ double pos_step(const KParams& P, double x, double v)
 // CUDA's ~100 for cos(); max error 2 ulp vs glibc over |p| <= 700 (1 ulp
 // near k*pi/2), the same class as CUDA's own cos -- the reference's glibc cos
 // is not reproducible bit for bit on the GPU either way.
+// The FP64 constants live in the constant bank: DFMA/DMUL read a c[][]
+// operand directly, whereas a 64-bit immediate costs two IMAD.MOV per use
+// (the d=32 rastrigin loop spent ~24 issue slots per cos on them).
+__constant__ double kCos[17] = {
+    0x1.8p52,                     // 0: rint shifter
+    6.36619772367581382433e-01,   // 1: 2/pi
+    1.57079632679489655800e+00,   // 2: pi/2 (Cody-Waite, 3 parts)
+    6.12323399573676603587e-17,   // 3
+    -1.49738490485916983212e-33,  // 4
+    -1.13596475577881948265e-11,  // 5: fdlibm __kernel_cos C6..C1
+    2.08757232129817482790e-09,   // 6
+    -2.75573143513906633035e-07,  // 7
+    2.48015872894767294178e-05,   // 8
+    -1.38888888888741095749e-03,  // 9
+    4.16666666666666019037e-02,   // 10
+    1.58969099521155010221e-10,   // 11: fdlibm __kernel_sin S6..S2
+    -2.50507602534068634195e-08,  // 12
+    2.75573137070700676789e-06,   // 13
+    -1.98412698298579493134e-04,  // 14
+    8.33333333332248946124e-03,   // 15
+    -1.66666666666666324348e-01,  // 16: S1
+};
+
+// fitness constants that are not 32-bit-immediate encodable (see kCos)
+__constant__ double kFitK[2] = {0.8, 6.283185307179586};
+
 __device__ __forceinline__ double cos_pso(double p) {
-  const double big = 0x1.8p52;
-  const double t = __fma_rn(p, 6.36619772367581382433e-01, big);  // rint(p * 2/pi) in the low bits
+  const double big = kCos[0];
+  const double t = __fma_rn(p, kCos[1], big);  // rint(p * 2/pi) in the low bits
   const double n = __dsub_rn(t, big);
   const uint32_t q = static_cast<uint32_t>(__double2loint(t)) & 3u;
-  double r = __fma_rn(-n, 1.57079632679489655800e+00, p);
-  r = __fma_rn(-n, 6.12323399573676603587e-17, r);
-  r = __fma_rn(-n, -1.49738490485916983212e-33, r);
+  double r = __fma_rn(-n, kCos[2], p);
+  r = __fma_rn(-n, kCos[3], r);
+  r = __fma_rn(-n, kCos[4], r);
   const double z = __dmul_rn(r, r);
   // cos kernel (fdlibm __kernel_cos, tail y = 0)
   const double cr = __dmul_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z,
-                        -1.13596475577881948265e-11, 2.08757232129817482790e-09), -2.75573143513906633035e-07),
-                        2.48015872894767294178e-05), -1.38888888888741095749e-03), 4.16666666666666019037e-02));
+                        kCos[5], kCos[6]), kCos[7]), kCos[8]), kCos[9]), kCos[10]));
   const double ar = fabs(r);
   const double qx = ar < 0.3 ? 0.0 : (ar > 0.78125 ? 0.28125 : __dmul_rn(ar, 0.25));
   const double hz = __dsub_rn(__dmul_rn(0.5, z), qx);
   const double kc = __dsub_rn(__dsub_rn(1.0, qx), __dsub_rn(hz, __dmul_rn(z, cr)));
   // sin kernel (fdlibm __kernel_sin, iy = 0)
-  const double sr = __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, 1.58969099521155010221e-10,
-                        -2.50507602534068634195e-08), 2.75573137070700676789e-06), -1.98412698298579493134e-04),
-                        8.33333333332248946124e-03);
-  const double ks = __dadd_rn(r, __dmul_rn(__dmul_rn(z, r), __fma_rn(z, sr, -1.66666666666666324348e-01)));
+  const double sr = __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, kCos[11], kCos[12]), kCos[13]), kCos[14]),
+                             kCos[15]);
+  const double ks = __dadd_rn(r, __dmul_rn(__dmul_rn(z, r), __fma_rn(z, sr, kCos[16])));
   const double v = (q & 1u) ? ks : kc;
   return (q == 1u || q == 2u) ? -v : v;
 }
 
 // ------------------------------------------------------------- fitness
 // Accumulators fed one axis at a time in ascending order (fitness.hpp:26-27).
+// add(v, axis) == accum(term(v, axis), v, axis) bit for bit: term() is the
+// per-axis work that does not depend on the running sum (the expensive cos of
+// griewank/rastrigin), accum() the strictly ordered fold. Split kernels compute
+// terms of different axes in different lanes and pass the accumulator along
+// (shfl_up) so the fold keeps the reference's order.
 enum FitId : int { kCubic = 0, kSphere = 1, kRosenbrock = 2, kGriewank = 3, kRastrigin = 4 };
 
 template <int F>
@@ -128,25 +157,34 @@ struct Fit;
 template <>
 struct Fit<kCubic> {  // fitness.hpp:47-54
   double acc = 0.0;
-  __device__ __forceinline__ void add(double v, uint32_t) {
-    const double t = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(__dsub_rn(v, 0.8), v), 1000.0), v), 8000.0);
-    acc = __dadd_rn(acc, t);
+  using Term = double;
+  __device__ __forceinline__ static Term term(double v, uint32_t) {
+    return __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(__dsub_rn(v, kFitK[0]), v), 1000.0), v), 8000.0);
   }
+  __device__ __forceinline__ void accum(Term t, double, uint32_t) { acc = __dadd_rn(acc, t); }
+  __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
   __device__ __forceinline__ double value() const { return acc; }
+  __device__ __forceinline__ void shfl_up(unsigned m, int w) { acc = __shfl_up_sync(m, acc, 1, w); }
 };
 
 template <>
 struct Fit<kSphere> {  // fitness.hpp:57-61
   double acc = 0.0;
-  __device__ __forceinline__ void add(double v, uint32_t) { acc = __dadd_rn(acc, __dmul_rn(v, v)); }
+  using Term = double;
+  __device__ __forceinline__ static Term term(double v, uint32_t) { return __dmul_rn(v, v); }
+  __device__ __forceinline__ void accum(Term t, double, uint32_t) { acc = __dadd_rn(acc, t); }
+  __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
   __device__ __forceinline__ double value() const { return -acc; }
+  __device__ __forceinline__ void shfl_up(unsigned m, int w) { acc = __shfl_up_sync(m, acc, 1, w); }
 };
 
 template <>
 struct Fit<kRosenbrock> {  // fitness.hpp:65-73: pairs (x_d, x_{d+1}) in ascending d
   double acc = 0.0;
   double prev = 0.0;
-  __device__ __forceinline__ void add(double v, uint32_t axis) {
+  struct Term {};
+  __device__ __forceinline__ static Term term(double, uint32_t) { return {}; }
+  __device__ __forceinline__ void accum(Term, double v, uint32_t axis) {
     if (axis > 0) {
       const double a = __dsub_rn(v, __dmul_rn(prev, prev));
       const double b = __dsub_rn(1.0, prev);
@@ -154,28 +192,47 @@ struct Fit<kRosenbrock> {  // fitness.hpp:65-73: pairs (x_d, x_{d+1}) in ascendi
     }
     prev = v;
   }
+  __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
   __device__ __forceinline__ double value() const { return -acc; }
+  __device__ __forceinline__ void shfl_up(unsigned m, int w) {
+    acc = __shfl_up_sync(m, acc, 1, w);
+    prev = __shfl_up_sync(m, prev, 1, w);
+  }
 };
 
 template <>
 struct Fit<kGriewank> {  // fitness.hpp:77-85 (cos_pso: <= 2 ulp from glibc)
   double sum = 0.0;
   double prod = 1.0;
-  __device__ __forceinline__ void add(double v, uint32_t axis) {
-    sum = __dadd_rn(sum, __ddiv_rn(__dmul_rn(v, v), 4000.0));
-    prod = __dmul_rn(prod, cos_pso(__ddiv_rn(v, __dsqrt_rn(static_cast<double>(axis + 1)))));
+  struct Term {
+    double s, c;
+  };
+  __device__ __forceinline__ static Term term(double v, uint32_t axis) {
+    return {__ddiv_rn(__dmul_rn(v, v), 4000.0), cos_pso(__ddiv_rn(v, __dsqrt_rn(static_cast<double>(axis + 1))))};
   }
+  __device__ __forceinline__ void accum(Term t, double, uint32_t) {
+    sum = __dadd_rn(sum, t.s);
+    prod = __dmul_rn(prod, t.c);
+  }
+  __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
   __device__ __forceinline__ double value() const { return -__dsub_rn(__dadd_rn(1.0, sum), prod); }
+  __device__ __forceinline__ void shfl_up(unsigned m, int w) {
+    sum = __shfl_up_sync(m, sum, 1, w);
+    prod = __shfl_up_sync(m, prod, 1, w);
+  }
 };
 
 template <>
 struct Fit<kRastrigin> {  // harness fitness_fn (oracle/pso_oracle.c:rastrigin)
   double acc = 0.0;
-  __device__ __forceinline__ void add(double v, uint32_t) {
-    const double t = __dadd_rn(__dsub_rn(__dmul_rn(v, v), __dmul_rn(10.0, cos_pso(__dmul_rn(6.283185307179586, v)))), 10.0);
-    acc = __dadd_rn(acc, t);
+  using Term = double;
+  __device__ __forceinline__ static Term term(double v, uint32_t) {
+    return __dadd_rn(__dsub_rn(__dmul_rn(v, v), __dmul_rn(10.0, cos_pso(__dmul_rn(kFitK[1], v)))), 10.0);
   }
+  __device__ __forceinline__ void accum(Term t, double, uint32_t) { acc = __dadd_rn(acc, t); }
+  __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
   __device__ __forceinline__ double value() const { return -acc; }
+  __device__ __forceinline__ void shfl_up(unsigned m, int w) { acc = __shfl_up_sync(m, acc, 1, w); }
 };
 
 // ------------------------------------------------------ (fit, idx) order

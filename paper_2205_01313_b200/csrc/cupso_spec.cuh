@@ -48,11 +48,174 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
+// A shard's summary of one pass (multi-GPU: all-gathered between ranks):
+// earliest admission seen, and the best candidate of the last iteration.
+struct SpecRec {
+  uint32_t tmin;      // ~0u: no admission before the last iteration
+  uint32_t admitted;  // admissions at the last iteration
+  double fit;         // best candidate of the last iteration (-inf / kNoParticle: none)
+  uint32_t particle;
+  uint32_t pad;
+  // followed by pos[d]
+};
+__host__ __device__ constexpr size_t spec_rec_bytes(uint32_t d) { return sizeof(SpecRec) + 8ull * d; }
+
+// The decision after a pass, identical on every rank (one block): the pass
+// failed if any shard saw an admission before its last iteration -> re-run
+// [t0, tmin] exactly; otherwise commit it: trace, snapshot (beats() among the
+// shards' candidates, each of which already beat the snapshot), occupancy, and
+// the next pass's schedule.
+__device__ void spec_decide(const KParams& P, const KCtl& C, SpecCtl* sc, const unsigned char* recs, uint32_t nrec,
+                            uint32_t t_end, uint32_t kmax) {
+  __shared__ uint32_t s_t0, s_K, s_fail;
+  __shared__ int s_w;
+  __shared__ double s_of;
+  __shared__ uint32_t s_oi;
+  const uint32_t tid = threadIdx.x;
+  const size_t rb = spec_rec_bytes(P.d);
+  if (tid == 0) {
+    const uint32_t t0 = ld_volatile_u32(&sc->t0), K = ld_volatile_u32(&sc->K);
+    const uint32_t par = ld_volatile_u32(&sc->parity), ks0 = ld_volatile_u32(&sc->kspec);
+    s_t0 = t0;
+    s_K = K;
+    s_fail = 0;
+    s_w = -1;
+    if (t0 < t_end) {
+      const uint32_t tl = t0 + K - 1;
+      uint32_t tm = ~0u;
+      double bf = -INFINITY;
+      uint32_t bi = kNoParticle;
+      unsigned long long adm = 0;
+      int w = -1;
+      for (uint32_t r = 0; r < nrec; ++r) {
+        const SpecRec* rec = reinterpret_cast<const SpecRec*>(recs + r * rb);
+        tm = min(tm, rec->tmin);
+        adm += rec->admitted;
+        if (rec->particle != kNoParticle && beats(rec->fit, rec->particle, bf, bi)) {
+          bf = rec->fit;
+          bi = rec->particle;
+          w = static_cast<int>(r);
+        }
+      }
+      s_of = C.snap->fit;
+      s_oi = C.snap->particle;
+      if (tm < tl) {  // speculation failed at tm: re-run [t0, tm] exactly from A
+        s_fail = 1;
+        sc->K = tm - t0 + 1;
+        sc->kspec = max(1u, ks0 / 2);
+        sc->fails += 1;
+      } else {
+        s_w = w;  // every candidate passed fit > snapshot: the winner is adopted
+        C.trace[tl] = w >= 0 ? bf : s_of;
+        C.trace_idx[tl] = w >= 0 ? bi : s_oi;
+        C.admitted[tl] = adm;
+        if (w >= 0) {
+          C.snap->fit = bf;
+          C.snap->particle = bi;
+        }
+        uint32_t ks = ks0;
+        if (K >= ks) ks = min(2 * ks, kmax);
+        const uint32_t tn = t0 + K;
+        sc->t0 = tn;
+        sc->parity = K == 1 ? par : (par ^ 1u);
+        sc->kspec = ks;
+        sc->K = tn < t_end ? min(ks, t_end - tn) : 0u;
+      }
+      sc->tmin = ~0u;
+      sc->passes += 1;
+    } else {
+      s_fail = 1;  // no pass ran: nothing to record
+    }
+  }
+  __syncthreads();
+  if (s_fail) return;
+  const uint32_t t0 = s_t0, tl = s_t0 + s_K - 1;
+  for (uint32_t t = t0 + tid; t < tl; t += blockDim.x) {
+    C.trace[t] = s_of;
+    C.trace_idx[t] = s_oi;
+  }
+  if (s_w >= 0) {
+    const double* rpos = reinterpret_cast<const double*>(recs + s_w * rb + sizeof(SpecRec));
+    for (uint32_t a = tid; a < P.d; a += blockDim.x) C.snap_pos[a] = rpos[a];
+  }
+}
+
+// Sharded passes: the decision over the all-gathered records (one block).
+__global__ void k_spec_commit(KParams P, KCtl C, SpecCtl* sc, const unsigned char* recs, uint32_t nrec,
+                              uint32_t t_end, uint32_t kmax) {
+  spec_decide(P, C, sc, recs, nrec, t_end, kmax);
+}
+
+// End of a pass (every block): block winner of the last iteration to the grid
+// queue; the last block to finish reduces the queue to this shard's SpecRec
+// (rec_out) and -- unless the pass is sharded (the host all-gathers the
+// records and runs k_spec_commit) -- takes the decision itself.
+template <int D>
+__device__ __forceinline__ void spec_finish(const KParams& P, const KState& So, const KCtl& C, SpecCtl* sc,
+                                            const uint32_t* s_ctl, BlockCand& bc, ResolveSmem& rs, int& s_last,
+                                            uint32_t t_end, uint32_t kmax, double snap_fit, double bf,
+                                            uint32_t bi, uint32_t adm, unsigned char* rec_out, int sharded) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t t0 = s_ctl[0], K = s_ctl[1];
+  const uint32_t tl = t0 + K - 1;
+  const size_t ld = P.ld;
+  warp_publish(bc, bf, bi, adm);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nq = bc.n;
+    if (nq) {  // block winner of iteration tl -> grid queue (position re-read from B)
+      double f = lane < nq ? bc.f[lane] : -INFINITY;
+      uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
+      warp_argmax(f, i);
+      uint32_t slot = 0;
+      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (lane == 0) {
+        C.q_fit[slot] = f;
+        C.q_idx[slot] = i;
+      }
+      for (uint32_t a = lane; a < D; a += 32)
+        C.q_pos[static_cast<size_t>(slot) * D + a] = So.pos[static_cast<size_t>(a) * ld + (i - P.base)];
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      if (bc.adm) atomicAdd(&C.admitted[tl], bc.adm);
+      s_last = last_block_done(C);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- the last block: this shard's record of the pass
+  __threadfence();
+  const uint32_t nq = __ldcg(&C.q_count[0]);
+  double wf = -INFINITY;
+  uint32_t wi = kNoParticle, ws = 0;
+  if (nq) resolve_queue(C, 0, nq, rs, wf, wi, ws);
+  SpecRec* rec = reinterpret_cast<SpecRec*>(rec_out);
+  double* rpos = reinterpret_cast<double*>(rec_out + sizeof(SpecRec));
+  for (uint32_t a = tid; a < D; a += blockDim.x)
+    rpos[a] = nq ? __ldcg(&C.q_pos[static_cast<size_t>(ws) * D + a]) : 0.0;
+  if (tid == 0) {
+    rec->tmin = ld_volatile_u32(&sc->tmin);
+    rec->admitted = static_cast<uint32_t>(__ldcg(&C.admitted[tl]));
+    rec->fit = wf;
+    rec->particle = nq ? wi : kNoParticle;
+    rec->pad = 0;
+    C.admitted[tl] = 0;  // the decision writes the total over shards
+    C.q_count[0] = 0;
+    __threadfence();
+  }
+  __syncthreads();
+  if (!sharded) spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
+}
+
 // D: dims (compile time; the particle's whole state lives in registers).
 // NP: adjacent particles per thread unit (2: LDG.128 / STG.128 on every row).
 template <int F, int D, int NP, int MINB>
 __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S0, KState S1, KCtl C,
-                                                            SpecCtl* sc, uint32_t t_end, uint32_t kmax) {
+                                                            SpecCtl* sc, uint32_t t_end, uint32_t kmax,
+                                                            unsigned char* rec_out, int sharded) {
   __shared__ double s_gpos[D];
   __shared__ BlockCand bc;
   __shared__ ResolveSmem rs;
@@ -166,80 +329,208 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
       }
     }
   }
-  warp_publish(bc, bf, bi, adm);
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t nq = bc.n;
-    if (nq) {  // block winner of iteration tl -> grid queue (position re-read from B)
-      double f = lane < nq ? bc.f[lane] : -INFINITY;
-      uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
-      warp_argmax(f, i);
-      uint32_t slot = 0;
-      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      if (lane == 0) {
-        C.q_fit[slot] = f;
-        C.q_idx[slot] = i;
-      }
-      for (uint32_t a = lane; a < D; a += 32)
-        C.q_pos[static_cast<size_t>(slot) * D + a] = So.pos[static_cast<size_t>(a) * ld + (i - P.base)];
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) {
-      if (bc.adm) atomicAdd(&C.admitted[tl], bc.adm);
-      s_last = last_block_done(C);
-    }
-  }
-  __syncthreads();
-  if (!s_last) return;
-  // ---- the last block resolves the pass and schedules the next one
-  __threadfence();
-  const uint32_t tm = ld_volatile_u32(&sc->tmin);
-  if (tm < tl) {  // speculation failed at tm: re-run [t0, tm] exactly from A
-    if (tid == 0) {
-      C.admitted[tl] = 0;
-      C.q_count[0] = 0;
-      sc->K = tm - t0 + 1;
-      sc->kspec = max(1u, s_ctl[3] / 2);
-      sc->tmin = ~0u;
-      sc->fails += 1;
-      sc->passes += 1;
-    }
-    return;
-  }
-  const uint32_t nq = __ldcg(&C.q_count[0]);
-  const double of = snap_fit;
-  const uint32_t oi = C.snap->particle;
-  double wf = of;
-  uint32_t wi = oi, ws = 0;
-  if (nq) {
-    resolve_queue(C, 0, nq, rs, wf, wi, ws);
-    for (uint32_t a = tid; a < D; a += blockDim.x)
-      C.snap_pos[a] = __ldcg(&C.q_pos[static_cast<size_t>(ws) * D + a]);
-  }
-  for (uint32_t t = t0 + tid; t < tl; t += blockDim.x) {
-    C.trace[t] = of;
-    C.trace_idx[t] = oi;
-  }
+  spec_finish<D>(P, So, C, sc, s_ctl, bc, rs, s_last, t_end, kmax, snap_fit, bf, bi, adm, rec_out, sharded);
+}
+
+// ------------------------------------------------ k_spec for wide swarms
+// d = DL * G: a particle is owned by G consecutive lanes, lane s of the group
+// holding axes [s*DL, s*DL + DL) in registers (cfg4: d = 32 = 8 x 4). Per
+// iteration every lane computes its axes' Philox draws, kinematics and
+// fitness terms (Fit<F>::term -- the cos of rastrigin/griewank included) in
+// parallel; the accumulator then travels up the group (shfl_up) and each lane
+// folds its terms in turn, so the sum keeps the reference's axis order bit for
+// bit. The fitness is broadcast from the group's last lane and every lane
+// makes the same pbest / snapshot decisions; lane 0 of the group speaks for
+// the particle (admissions, candidates). Warps stay converged (partial groups
+// at the swarm's end compute neutral state), so every shuffle is full-mask.
+// SM: keep each lane's x / v / pbest columns and its fitness terms in shared
+// memory (a private column per thread, stride blockDim: conflict-free) instead
+// of registers -- fewer live registers, so more resident warps and no spills
+// for the cos-heavy fitnesses; dynamic SMEM = (3 + term width) * DL * blockDim
+// doubles.
+template <int F, int DL, int G, int MINB, bool SM = false>
+__global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KState S0, KState S1, KCtl C,
+                                                                  SpecCtl* sc, uint32_t t_end, uint32_t kmax,
+                                                                  unsigned char* rec_out, int sharded) {
+  constexpr int D = DL * G;
+  extern __shared__ double s_state[];
+  static_assert(32 % G == 0, "G must divide the warp");
+  __shared__ double s_gpos[D];
+  __shared__ BlockCand bc;
+  __shared__ ResolveSmem rs;
+  __shared__ uint32_t s_ctl[4];
+  __shared__ int s_last;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t sub = lane % G;
   if (tid == 0) {
-    C.trace[tl] = wf;  // every queue entry passed fit > snapshot: the winner is adopted
-    C.trace_idx[tl] = wi;
-    if (nq) {
-      C.snap->fit = wf;
-      C.snap->particle = wi;
-    }
-    C.q_count[0] = 0;
-    uint32_t ks = s_ctl[3];
-    if (K >= ks) ks = min(2 * ks, kmax);
-    const uint32_t tn = t0 + K;
-    sc->t0 = tn;
-    sc->parity = inplace ? par : (par ^ 1u);
-    sc->kspec = ks;
-    sc->K = tn < t_end ? min(ks, t_end - tn) : 0u;
-    sc->tmin = ~0u;
-    sc->passes += 1;
+    s_ctl[0] = ld_volatile_u32(&sc->t0);
+    s_ctl[1] = ld_volatile_u32(&sc->K);
+    s_ctl[2] = ld_volatile_u32(&sc->parity);
+    s_ctl[3] = ld_volatile_u32(&sc->kspec);
+    bc.n = 0;
+    bc.adm = 0;
   }
+  for (uint32_t a = tid; a < D; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  __syncthreads();
+  const uint32_t t0 = s_ctl[0], K = s_ctl[1], par = s_ctl[2];
+  if (t0 >= t_end) return;
+  const bool inplace = K == 1;
+  const KState Si = par ? S1 : S0;
+  const KState So = inplace ? Si : (par ? S0 : S1);
+  const double snap_fit = C.snap->fit;
+  const uint32_t tl = t0 + K - 1;
+  const uint32_t a0 = sub * DL;  // first axis of this lane
+  double gp[DL];
+#pragma unroll
+  for (int a = 0; a < DL; ++a) gp[a] = s_gpos[a0 + a];
+  double bf = -INFINITY;
+  uint32_t bi = kNoParticle, adm = 0;
+  uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
+  const uint32_t per_warp = 32 / G;
+  const uint32_t stride = gridDim.x * (blockDim.x / G);
+  const size_t ld = P.ld;
+  // warp-uniform particle loop: particle = u0 + lane / G
+  for (uint32_t u0 = (blockIdx.x * blockDim.x + (tid & ~31u)) / G; u0 < P.n; u0 += stride) {
+    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+    uint32_t te = min(t0 + K, tstop);
+    if (te <= t0) break;  // warp-uniform: one load serves the warp
+    const uint32_t li = u0 + lane / G;
+    const bool live = li < P.n;
+    const uint32_t gi = P.base + li;
+    double rx[SM ? 1 : DL], rv[SM ? 1 : DL], rpb[SM ? 1 : DL], pbf = -INFINITY;
+    const uint32_t bd = blockDim.x;
+    auto X = [&](int a) -> double& {
+      if constexpr (SM) return s_state[(0 * DL + a) * bd + tid]; else return rx[a];
+    };
+    auto V = [&](int a) -> double& {
+      if constexpr (SM) return s_state[(1 * DL + a) * bd + tid]; else return rv[a];
+    };
+    auto PB = [&](int a) -> double& {
+      if constexpr (SM) return s_state[(2 * DL + a) * bd + tid]; else return rpb[a];
+    };
+    if (live) {
+#pragma unroll
+      for (int a = 0; a < DL; ++a) {
+        const size_t at = static_cast<size_t>(a0 + a) * ld + li;
+        X(a) = Si.pos[at];
+        V(a) = Si.vel[at];
+        PB(a) = Si.pb[at];
+      }
+      pbf = Si.pbf[li];
+    } else {
+#pragma unroll
+      for (int a = 0; a < DL; ++a) X(a) = V(a) = PB(a) = 0.0;
+    }
+    uint32_t t = t0;
+    bool bad = false, dirty = false;
+    for (; t < te; ++t) {
+      Fit<F> acc;
+      if constexpr (SM) {
+        // axes one (two) at a time: x/v/pbest and the terms stay in SMEM, so
+        // only ~2 axes' Philox chains are live -> no spills at 3-4 blocks/SM
+        using Term = typename Fit<F>::Term;
+        constexpr int TW = (sizeof(Term) + 7) / 8;
+        double* tcol = s_state + (3 * DL) * bd + tid;  // TW * DL doubles, stride bd
+#pragma unroll 2
+        for (int a = 0; a < DL; ++a) {
+          const double r1 = uniform01(P, t, gi, a0 + a, 0);
+          const double r2 = uniform01(P, t, gi, a0 + a, 1);
+          const double x0 = X(a);
+          const double nv = vel_step(P, V(a), x0, PB(a), s_gpos[a0 + a], r1, r2);
+          const double nx = pos_step(P, x0, nv);
+          V(a) = nv;
+          X(a) = nx;
+          if constexpr (sizeof(Term) >= 8) {
+            const Term tv = Fit<F>::term(nx, a0 + a);
+            double w[TW];
+            memcpy(w, &tv, sizeof(Term));
+#pragma unroll
+            for (int q = 0; q < TW; ++q) tcol[(a * TW + q) * bd] = w[q];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          if (q > 0) acc.shfl_up(0xffffffffu, G);
+          if (sub == static_cast<uint32_t>(q)) {
+            for (int a = 0; a < DL; ++a) {
+              Term tv{};
+              if constexpr (sizeof(Term) >= 8) {
+                double w[TW];
+#pragma unroll
+                for (int z = 0; z < TW; ++z) w[z] = tcol[(a * TW + z) * bd];
+                memcpy(&tv, w, sizeof(Term));
+              }
+              acc.accum(tv, X(a), a0 + a);
+            }
+          }
+        }
+      } else {
+        typename Fit<F>::Term tm[DL];
+        double xs[F == kRosenbrock ? DL : 1];  // rosenbrock's fold needs the positions
+#pragma unroll
+        for (int a = 0; a < DL; ++a) {
+          const double r1 = uniform01(P, t, gi, a0 + a, 0);
+          const double r2 = uniform01(P, t, gi, a0 + a, 1);
+          const double x0 = X(a);
+          const double nv = vel_step(P, V(a), x0, PB(a), gp[a], r1, r2);
+          const double nx = pos_step(P, x0, nv);
+          V(a) = nv;
+          X(a) = nx;
+          tm[a] = Fit<F>::term(nx, a0 + a);
+          if constexpr (F == kRosenbrock) xs[a] = nx;
+        }
+        // ordered fold across the group: lane s folds after lane s-1
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          if (q > 0) acc.shfl_up(0xffffffffu, G);
+          if (sub == static_cast<uint32_t>(q)) {
+#pragma unroll
+            for (int a = 0; a < DL; ++a) acc.accum(tm[a], F == kRosenbrock ? xs[a] : 0.0, a0 + a);
+          }
+        }
+      }
+      const double f = __shfl_sync(0xffffffffu, acc.value(), G - 1, G);
+      if (live && f > pbf) {  // update_pbest (swarm.hpp:100-108)
+        dirty = true;
+        pbf = f;
+#pragma unroll
+        for (int a = 0; a < DL; ++a) PB(a) = X(a);
+      }
+      bool early = false;
+      if (live && f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+        if (t < tl) {
+          early = true;
+        } else if (sub == 0) {
+          ++adm;
+          if (beats(f, gi, bf, bi)) {
+            bf = f;
+            bi = gi;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, early)) {  // the pass is falsified at t
+        if (lane == 0) atomicMin(&sc->tmin, t);
+        tstop = t;
+        bad = true;
+        break;
+      }
+      if (((t - t0) & 15u) == 15u) {
+        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+        te = min(te, tstop);
+      }
+    }
+    if (!bad && t == t0 + K && live) {
+#pragma unroll
+      for (int a = 0; a < DL; ++a) {
+        const size_t at = static_cast<size_t>(a0 + a) * ld + li;
+        So.pos[at] = X(a);
+        So.vel[at] = V(a);
+        if (!inplace || dirty) So.pb[at] = PB(a);
+      }
+      if (sub == 0 && (!inplace || dirty)) So.pbf[li] = pbf;
+    }
+  }
+  spec_finish<D>(P, So, C, sc, s_ctl, bc, rs, s_last, t_end, kmax, snap_fit, bf, bi, adm, rec_out, sharded);
 }
 
 }  // namespace cupso

@@ -117,16 +117,21 @@ class Swarm:
     def sync_grid_blocks(self) -> int:
         return lib().cupso_sync_grid_blocks(self._h)
 
-    SYNC_MODES = {0: "undecided", 1: "persistent", 2: "wave", 3: "resident", 4: "nccl-sharded", 5: "spec"}
+    SYNC_MODES = {0: "undecided", 1: "persistent", 2: "wave", 3: "resident", 4: "nccl-sharded", 5: "spec", 6: "nccl-sharded-spec"}
 
     def sync_mode(self) -> str:
         return self.SYNC_MODES[lib().cupso_sync_mode(self._h)]
 
-    def spec_stats(self) -> tuple[int, int]:
-        """(passes, falsified passes) of the speculative cuda-sync mode on this handle."""
-        a, b = C.c_uint64(0), C.c_uint64(0)
-        check(lib().cupso_spec_stats(self._h, C.byref(a), C.byref(b)))
-        return a.value, b.value
+    def spec_stats(self) -> tuple[int, int, int]:
+        """(passes, falsified passes, launches) of the speculative cuda-sync mode on this handle."""
+        a, b, c = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        check(lib().cupso_spec_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    ASYNC_MODES = {0: "undecided", 1: "plain", 2: "tiled", 3: "reg"}
+
+    def async_mode(self) -> str:
+        return self.ASYNC_MODES[lib().cupso_async_mode(self._h)]
 
     def stream(self) -> int:
         return lib().cupso_stream(self._h) or 0
@@ -218,3 +223,23 @@ def select_winner(records: list[tuple[float, int]], snap_fit: float) -> int:
         if f > bf or (f == bf and i < bi):
             best, bf, bi = k, f, i
     return best if best >= 0 and bf > snap_fit else -1
+
+
+def spec_decide(records, t0: int, K: int, kspec: int, kmax: int, t_end: int) -> dict:
+    """Host mirror of spec_decide (csrc/cupso_spec.cuh): the decision every rank
+    takes after a speculative pass over [t0, t0+K) from the all-gathered shard
+    records (tmin, admitted, fit, particle). Returns the winner's record index
+    (-1: none), whether the pass failed, and the next pass's (t0, K, kspec)."""
+    tl = t0 + K - 1
+    tm = min(r[0] for r in records)
+    if tm < tl:  # an admission before the last iteration: re-run [t0, tm] exactly
+        return dict(failed=True, winner=-1, t0=t0, K=tm - t0 + 1, kspec=max(1, kspec // 2),
+                    admitted=0)
+    w, bf, bi = -1, -np.inf, NO_PARTICLE
+    for k, (_, _, f, i) in enumerate(records):
+        if i != NO_PARTICLE and (f > bf or (f == bf and i < bi)):
+            w, bf, bi = k, f, i
+    ks = min(2 * kspec, kmax) if K >= kspec else kspec
+    tn = t0 + K
+    return dict(failed=False, winner=w, t0=tn, K=min(ks, t_end - tn) if tn < t_end else 0, kspec=ks,
+                admitted=sum(r[1] for r in records))

@@ -45,19 +45,26 @@ def test_shards_with_host_exchange_equal_single_swarm(cupso, fitness, n, d, T, s
             sh.close()
 
 
-def test_nccl_single_rank_exchange(cupso):
-    """The NCCL-backed sharded step (propose -> ncclAllGather -> commit on the
-    shard's stream) with one rank equals the persistent kernel."""
+@pytest.mark.parametrize("mode,d,want", [("auto", 4, "nccl-sharded-spec"), ("auto", 32, "nccl-sharded-spec"),
+                                         ("wave", 4, "nccl-sharded"), ("auto", 3, "nccl-sharded")])
+def test_nccl_single_rank_exchange(cupso, oracle, monkeypatch, mode, d, want):
+    """The NCCL-backed sharded step with one rank -- per iteration (propose ->
+    ncclAllGather -> commit) or per speculative pass (k_spec -> ncclAllGather of
+    a SpecRec -> k_spec_commit) on the shard's stream -- reproduces run_serial."""
+    monkeypatch.setenv("CUPSO_SYNC_MODE", mode)
     f = cupso.find_fitness("sphere")
-    p = cupso.make_params(f, 3000, 4, 30)
-    with cupso.Swarm(p, f, 5) as a:
-        a.step(cupso.SYNC, 30)
-        ta, pa, _ = a.trace()
+    n, T = 3000, 40
+    p = cupso.make_params(f, n, d, T)
     with cupso.Swarm(p, f, 5) as b:
         b.nccl_init(cupso.nccl_unique_id(), 1, 0)
-        b.step(cupso.SYNC, 30)
+        b.step(cupso.SYNC, 17)
+        b.step(cupso.SYNC, T - 17)
+        assert b.sync_mode() == want
         tb, pb, _ = b.trace()
-    assert same(ta, tb) and np.array_equal(pa, pb)
+        st = b.state()
+    ref = oracle.run_serial("sphere", n, d, T, 5)
+    assert same(tb, ref.trace) and np.array_equal(pb, ref.trace_particle)
+    assert same(st.positions, ref.state["positions"]) and same(st.pbest_fit, ref.state["pbest_fit"])
 
 
 def test_sync_modes_agree(cupso, monkeypatch):

@@ -43,7 +43,7 @@ def compare_state(got, orc, fit, what):
             assert_close(getattr(got, k), orc.state[k], f"{what} {k}")
 
 
-@pytest.mark.parametrize("d", [1, 2, 4, 8])
+@pytest.mark.parametrize("d", [1, 2, 4, 8, 16, 32, 64])
 @pytest.mark.parametrize("fit", FITNESS)
 def test_spec_matches_oracle(cupso, oracle, spec_env, fit, d):
     n, T, seed = 3001, 120, 11  # odd n: the last two-particle unit is half padding
@@ -56,8 +56,8 @@ def test_spec_matches_oracle(cupso, oracle, spec_env, fit, d):
         gbest_pos, gbest_particle = got["gbest"].pos, got["gbest"].particle
     compare_run(R, orc, fit, f"spec {fit} d={d}")
     compare_state(got["state"], orc, fit, f"spec {fit} d={d}")
-    passes, fails = got["stats"]
-    assert 0 < passes <= T + fails
+    passes, fails, launches = got["stats"]
+    assert 0 < passes <= T + fails and launches >= passes
 
 
 @pytest.mark.parametrize("kmax", ["1", "2", "7", "64"])
@@ -69,7 +69,7 @@ def test_spec_pass_length_invariance(cupso, oracle, spec_env, kmax):
     assert_bitwise(got["trace"], orc.trace, f"K={kmax} trace")
     assert np.array_equal(got["trace_particle"], orc.trace_particle)
     compare_state(got["state"], orc, "sphere", f"K={kmax}")
-    passes, fails = got["stats"]
+    passes, fails, launches = got["stats"]
     if kmax == "1":
         assert fails == 0 and passes == T  # K = 1 passes are exact by construction
     else:
@@ -96,7 +96,7 @@ def test_spec_speculation_is_falsified_and_recovered(cupso, oracle, spec_env):
     """A swarm whose gbest keeps improving: many passes fail and are re-run, result exact."""
     n, d, T, seed = 20000, 2, 200, 3
     got = run_sync(cupso, "rosenbrock", n, d, T, seed)
-    passes, fails = got["stats"]
+    passes, fails, launches = got["stats"]
     orc = oracle.run_serial("rosenbrock", n, d, T, seed)
     changes = int(np.count_nonzero(np.diff(orc.trace) != 0))
     assert changes > 3 and fails > 0, (changes, fails)
@@ -141,6 +141,23 @@ def test_spec_single_particle_and_single_iteration(cupso, oracle, spec_env):
         orc = oracle.run_serial("sphere", n, 1, T, 9)
         assert_bitwise(got["trace"], orc.trace, f"n={n} T={T}")
         compare_state(got["state"], orc, "sphere", f"n={n} T={T}")
+
+
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7"])
+def test_spec_split_tunings_agree(cupso, oracle, monkeypatch, cfg):
+    """d = 32 (the cfg4 shape): every lanes-per-particle split of k_spec_split is bit-identical."""
+    monkeypatch.setenv("CUPSO_SYNC_MODE", "spec")
+    monkeypatch.setenv("CUPSO_SPEC_CFG", cfg)
+    n, d, T, seed = 2049, 32, 60, 4
+    got = run_sync(cupso, "rastrigin", n, d, T, seed)
+    assert got["mode"] == "spec"
+    orc = oracle.run_serial("rastrigin", n, d, T, seed)
+    assert np.array_equal(got["trace_particle"], orc.trace_particle)
+    compare_state(got["state"], orc, "rastrigin", f"cfg {cfg}")
+    got_c = run_sync(cupso, "cubic", n, d, T, seed)
+    orc_c = oracle.run_serial("cubic", n, d, T, seed)
+    assert_bitwise(got_c["trace"], orc_c.trace, "cubic trace")
+    compare_state(got_c["state"], orc_c, "cubic", f"cfg {cfg}")
 
 
 def test_spec_cfg5_shape_equals_wave(cupso, monkeypatch):
