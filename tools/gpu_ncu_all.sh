@@ -23,3 +23,7 @@ run cfg5proxy_spec k_spec 0 40 "CUPSO_SYNC_MODE=spec" cuda-sync sphere 24 8 20
 run cfg5proxy_wave k_wave 5 1 "CUPSO_SYNC_MODE=wave" cuda-sync sphere 24 8 10
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 3 --warmup 3 --no-cpu > /dev/null 2>&1
 ls -la gpurun_out/*.ncu-rep | wc -l
+# summaries travel back; the large multi-launch reports do not (gpurun_out <= 64 MiB)
+python tools/make_profiles.py r01 gpurun_out/profiles_r01
+for f in gpurun_out/*.ncu-rep; do [ $(stat -c %s "$f") -gt 6000000 ] && rm -f "$f"; done
+du -sh gpurun_out

@@ -35,7 +35,9 @@ CAPTURES = {
 }
 
 
-def main(tag):
+def main(tag, dest=None):
+    """dest: directory for the summaries (default profiles/; on the GPU box use gpurun_out/... so they travel)."""
+    pdir = dest or os.path.join(ROOT, "profiles")
     lines = [f"# {tag}: ncu --set full --clock-control none captures (B200, sm_100a); one launch each",
              "# per-launch numbers are cold-cache and serialised under replay; compare shares, not absolutes", ""]
     js = {}
@@ -74,10 +76,10 @@ def main(tag):
                 lines.append(f"-- {key}: {n} launches, {iters} iterations: dram {(tot['rd'] + tot['wr']) / iters / 1e6:.1f} MB/iter, "
                              f"{tot['inst'] / iters / 1e6:.1f} M warp-inst/iter, {tot['ms']:.3f} ms total (serialised replay)")
                 lines.append("")
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w") as fh:
+    os.makedirs(pdir, exist_ok=True)
+    with open(os.path.join(pdir, f"{tag}_ncu_summary.txt"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    with open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.json"), "w") as fh:
+    with open(os.path.join(pdir, f"ncu_summary_{tag}.json"), "w") as fh:
         json.dump(js, fh, indent=1)
     # launch list of the default bench command
     lp = os.path.join(OUT, "launches_cfg2.csv")
@@ -104,9 +106,9 @@ def main(tag):
                f"# {'launches':>8} {'total_us':>12} {'share':>6}  kernel"]
         for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             out.append(f"  {c:8d} {t / 1e3:12.1f} {100 * t / tot:5.1f}%  {n}")
-        with open(os.path.join(ROOT, "profiles", f"{tag}_launches_cfg2.txt"), "w") as fh:
+        with open(os.path.join(pdir, f"{tag}_launches_cfg2.txt"), "w") as fh:
             fh.write("\n".join(out) + "\n")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", sys.argv[2] if len(sys.argv) > 2 else None)
