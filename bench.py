@@ -325,11 +325,12 @@ def main():
     grid = sw.sync_grid_blocks()
 
     # ---- roofline of the dominant kernel (one launch = T iterations for the persistent kernels) ----
-    bytes_per_pu = (5 * d + 1) * 8
+    f32 = variant_name == "cuda-sync-f32"
+    bytes_per_pu = (5 * d + 1) * (4 if f32 else 8)
     # cuda-sync runs as speculative passes (k_spec: ~T/K launches per step),
     # persistent (1 cooperative launch per step) or as a graph of one wave per
     # iteration; shards: propose+commit per iteration
-    mode = sw.sync_mode() if variant_name == "cuda-sync" else None
+    mode = sw.sync_mode() if variant_name == "cuda-sync" else ("spec" if f32 else None)
     amode = sw.async_mode() if variant_name == "cuda-async" else None
     spec1 = sw.spec_stats()
     spec_passes = (spec1[0] - spec0[0]) / K
@@ -341,7 +342,7 @@ def main():
     launches_per_step = {"cuda-sync": (spec_launches * (2 if world > 1 else 1)) if spec else
                          (1 if persistent else (2 * T if world > 1 else T)), "cuda-async": 1,
                          "cuda-queue-lock": T, "cuda-queue": 2 * T, "cuda-reduction": 2 * T,
-                         "cuda-unrolled": 2 * T}[variant_name]
+                         "cuda-unrolled": 2 * T, "cuda-sync-f32": spec_launches}[variant_name]
     iters_per_launch = T if persistent else (T / spec_passes if spec else 1)
     launch_secs = (dev_secs / K) / (T / iters_per_launch)
     alg_bytes = count * iters_per_launch * bytes_per_pu
@@ -354,11 +355,13 @@ def main():
                    "wave": f"k_wave<{fitness}>", "spec": f"k_spec<{fitness},{d}>",
                    "nccl-sharded-spec": f"k_spec<{fitness},{d}>+k_spec_commit"}.get(
                        mode, f"k_propose<{fitness}>+k_commit")
+    if f32:
+        sync_kernel = f"k_spec32<{fitness},{d}>"
     async_kernel = {"reg": f"k_async_reg<{fitness},{d}>", "tiled": f"k_async_tiled<{fitness}>"}.get(
         amode, f"k_async<{fitness}>")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": {"cuda-sync": sync_kernel,
+                "kernel": {"cuda-sync": sync_kernel, "cuda-sync-f32": sync_kernel,
                            "cuda-async": async_kernel}.get(variant_name, f"k_classic_step<{fitness}>"),
                 "mode": mode or amode,
                 "traffic_note": "ncu dram read+write per launch (profiles/ncu_summary_r01.json); "
@@ -458,7 +461,8 @@ def main():
         line = {
             "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
             "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * dev_secs / K,
-            "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak", "vs_baseline": None,
+            "dtype": "f32" if f32 else "f64",
             "data": "synthetic (Philox-initialised swarm, reference make_params defaults)",
             "config": {"workload": desc, "fitness": fitness, "particles_total": n_total,
                        "particles_per_gpu": count, "dims": d, "iterations_per_step": T,

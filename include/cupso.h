@@ -62,7 +62,9 @@ typedef enum cupso_variant {
   CUPSO_QUEUE = 2,      /* "cuda-queue"    : filtered smem queue + fold     (engine_queue.hpp:39-78) */
   CUPSO_QUEUE_LOCK = 3, /* "cuda-queue-lock": fused, lock-guarded commit   (engine_queue.hpp:86-104) */
   CUPSO_SYNC = 4,       /* "cuda-sync"     : persistent fused kernel, grid queue + grid barrier */
-  CUPSO_ASYNC = 5       /* "cuda-async"    : persistent free-running blocks, CAS/seqlock gbest */
+  CUPSO_ASYNC = 5,      /* "cuda-async"    : persistent free-running blocks, CAS/seqlock gbest */
+  CUPSO_SYNC_F32 = 6    /* "cuda-sync-f32" : FP32 state, packed 64-bit (fitness, index) atomicMax
+                           aggregation; statistical (not bitwise) vs the FP64 reference */
 } cupso_variant;
 
 /* Read-only view handed to an observer (engine.hpp:29-30 iteration_observer).

@@ -5,7 +5,7 @@ find_fitness, engine_registry, find_engine, run_result, ...) on top of
 libcupso.so, whose C-ABI is declared in include/cupso.h. Importing the package
 does not require a GPU; running an engine does (no CPU fallback).
 """
-from ._lib import (ASYNC, QUEUE, QUEUE_LOCK, REDUCTION, SYNC, UNROLLED, CupsoError, DomainError,
+from ._lib import (ASYNC, QUEUE, QUEUE_LOCK, REDUCTION, SYNC, SYNC_F32, UNROLLED, CupsoError, DomainError,
                    LogicError, lib)
 from .engine import (FIT_SENTINEL, NO_PARTICLE, device_count, engine_entry, engine_registry,
                      exec_options, find_engine, find_fitness, fitness_fn, fitness_registry,

@@ -13,7 +13,7 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CUPSO_LIB") or os.path.join(PKG_DIR, "libcupso.so")
 
 CUPSO_OK, CUPSO_EINVAL, CUPSO_ERUNTIME, CUPSO_ELOGIC, CUPSO_EDOMAIN, CUPSO_ECUDA = range(6)
-REDUCTION, UNROLLED, QUEUE, QUEUE_LOCK, SYNC, ASYNC = range(6)
+REDUCTION, UNROLLED, QUEUE, QUEUE_LOCK, SYNC, ASYNC, SYNC_F32 = range(7)
 
 
 class cupso_params(C.Structure):

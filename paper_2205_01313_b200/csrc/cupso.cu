@@ -24,6 +24,7 @@
 #include "../../include/cupso.h"
 #include "cupso_kernels.cuh"
 #include "cupso_spec.cuh"
+#include "cupso_f32.cuh"
 
 using namespace cupso;
 
@@ -61,9 +62,9 @@ const double kFitLo[] = {-100.0, -100.0, -2.048, -600.0, -5.12};
 const double kFitHi[] = {100.0, 100.0, 2.048, 600.0, 5.12};
 constexpr int kNumFit = 5;
 
-const char* const kVarNames[] = {"cuda-reduction", "cuda-unrolled", "cuda-queue",
-                                 "cuda-queue-lock", "cuda-sync",    "cuda-async"};
-constexpr int kNumVar = 6;
+const char* const kVarNames[] = {"cuda-reduction", "cuda-unrolled", "cuda-queue", "cuda-queue-lock",
+                                 "cuda-sync",      "cuda-async",    "cuda-sync-f32"};
+constexpr int kNumVar = 7;
 
 // std::to_string(double) == "%f" (params.hpp:38-42 message text)
 std::string fstr(double v) {
@@ -174,6 +175,15 @@ struct cupso_swarm {
   unsigned char* spec_rec_local = nullptr;  // this shard's SpecRec of the running pass
   unsigned char* spec_rec_all = nullptr;    // [nranks] all-gathered records (sharded)
   uint64_t spec_passes = 0, spec_fails = 0, spec_launches = 0;
+  // FP32 engine (cuda-sync-f32): its own double-buffered FP32 state; the
+  // FP64 state stays authoritative for every other entry point (f32_active:
+  // the FP32 copy is newer and must be converted back before FP64 use)
+  bool f32_ready = false, f32_active = false;
+  KState32 S32{}, S32_alt{};
+  KParams32 Q{};
+  SpecCtl32* spec32_ctl = nullptr;
+  const void* f32_kfn = nullptr;
+  int f32_grid = 0;
   bool areg_checked = false;   // register-resident cuda-async probed
   int areg_grid = 0, areg_k = 32;
   std::vector<int> async_iters;         // iterations produced by the async variant (trace decode)
@@ -704,7 +714,7 @@ bool spec_fits(cupso_swarm* h) {
       cudaMalloc(&pb, cells * 8) != cudaSuccess || cudaMalloc(&pbf, h->P.ld * 8) != cudaSuccess ||
       cudaMalloc(&ctl, sizeof(SpecCtl)) != cudaSuccess || cudaMalloc(&rl, rb) != cudaSuccess ||
       cudaMalloc(&ra, rb * std::max(1, h->nranks)) != cudaSuccess ||
-      cudaMallocHost(&host, sizeof(SpecCtl)) != cudaSuccess) {
+      (!h->spec_host && cudaMallocHost(&host, sizeof(SpecCtl)) != cudaSuccess)) {
     for (void* p : {pos, vel, pb, pbf, ctl, rl, ra}) cudaFree(p);
     if (host) cudaFreeHost(host);
     cudaGetLastError();
@@ -716,7 +726,7 @@ bool spec_fits(cupso_swarm* h) {
   h->S_alt = KState{static_cast<double*>(pos), static_cast<double*>(vel), static_cast<double*>(pb),
                     static_cast<double*>(pbf)};
   h->spec_ctl = static_cast<SpecCtl*>(ctl);
-  h->spec_host = static_cast<SpecCtl*>(host);
+  if (host) h->spec_host = static_cast<SpecCtl*>(host);
   if (ensure_queue(h, grid) != CUPSO_OK) return false;
   const char* ke = getenv("CUPSO_SPEC_K");
   h->spec_kmax = ke ? std::max(1, atoi(ke)) : 64;
@@ -893,6 +903,126 @@ cupso_status sharded_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   return CUPSO_OK;
 }
 
+// ----------------------------------------------------------- FP32 engine
+template <int F, int D>
+const void* f32_kernel(int* np) {
+  constexpr int NP = D <= 2 ? 4 : (D == 4 ? 2 : 1);
+  *np = NP;
+  return reinterpret_cast<const void*>(k_spec32<F, D, NP, D == 8 ? 2 : 3>);
+}
+
+cupso_status ensure_f32(cupso_swarm* h) {
+  if (h->f32_ready) return CUPSO_OK;
+  const size_t cells = h->P.ld * h->P.d;
+  void* p[8];
+  for (int k = 0; k < 2; ++k) {
+    TRY(dmalloc(h, &p[4 * k + 0], cells * 4));
+    TRY(dmalloc(h, &p[4 * k + 1], cells * 4));
+    TRY(dmalloc(h, &p[4 * k + 2], cells * 4));
+    TRY(dmalloc(h, &p[4 * k + 3], h->P.ld * 4));
+  }
+  h->S32 = KState32{static_cast<float*>(p[0]), static_cast<float*>(p[1]), static_cast<float*>(p[2]),
+                    static_cast<float*>(p[3])};
+  h->S32_alt = KState32{static_cast<float*>(p[4]), static_cast<float*>(p[5]), static_cast<float*>(p[6]),
+                        static_cast<float*>(p[7])};
+  void* c;
+  TRY(dmalloc(h, &c, sizeof(SpecCtl32)));
+  CK(cudaMemset(c, 0, sizeof(SpecCtl32)));
+  h->spec32_ctl = static_cast<SpecCtl32*>(c);
+  if (!h->spec_rec_local) {
+    void* rl;
+    TRY(dmalloc(h, &rl, spec_rec_bytes(h->P.d)));
+    h->spec_rec_local = static_cast<unsigned char*>(rl);
+  }
+  const KParams& P = h->P;
+  h->Q = KParams32{static_cast<float>(P.w), static_cast<float>(P.c1), static_cast<float>(P.c2),
+                   static_cast<float>(P.min_pos), static_cast<float>(P.max_pos), static_cast<float>(P.min_v),
+                   static_cast<float>(P.max_v)};
+  int np = 1;
+  dispatch_fit(h->fid, [&](auto F) {
+    constexpr int f = decltype(F)::value;
+    switch (h->P.d) {
+      case 1: h->f32_kfn = f32_kernel<f, 1>(&np); break;
+      case 2: h->f32_kfn = f32_kernel<f, 2>(&np); break;
+      case 4: h->f32_kfn = f32_kernel<f, 4>(&np); break;
+      case 8: h->f32_kfn = f32_kernel<f, 8>(&np); break;
+      default: h->f32_kfn = nullptr;  // any other dims: k_wave32, one launch per iteration
+    }
+  });
+  if (h->f32_kfn) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->f32_kfn, kSyncThreads, 0));
+    if (per_sm < 1) return fail(CUPSO_ECUDA, "cuda-sync-f32: kernel cannot be resident");
+    const uint64_t units = (h->P.n + np - 1ull) / np;
+    const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
+    const uint64_t rounds = (units + resident - 1) / resident;
+    const uint64_t threads = (units + rounds - 1) / rounds;
+    h->f32_grid = static_cast<int>(std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads));
+  } else {
+    h->f32_grid = static_cast<int>(std::min<uint64_t>((h->P.n + kSyncThreads - 1) / kSyncThreads,
+                                                     static_cast<uint64_t>(num_sms(h->device)) * 8));
+  }
+  h->f32_ready = true;
+  return CUPSO_OK;
+}
+
+int conv_blocks(const cupso_swarm* h) {
+  return static_cast<int>(std::min<uint64_t>((h->P.ld * h->P.d + 255) / 256, 148ull * 16));
+}
+
+// FP32 copy newer than the FP64 state: convert back (any FP64 consumer calls this).
+cupso_status sync_f64(cupso_swarm* h) {
+  if (!h->f32_active) return CUPSO_OK;
+  CK(cudaSetDevice(h->device));
+  k_to_f64<<<conv_blocks(h), 256, 0, h->stream>>>(h->P, h->S32, h->S);
+  CK(cudaGetLastError());
+  h->f32_active = false;
+  return CUPSO_OK;
+}
+
+cupso_status f32_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
+  if (!h->f32_kfn) {  // generic dims: one k_wave32 launch per iteration
+    cudaError_t e = cudaSuccess;
+    dispatch_fit(h->fid, [&](auto F) {
+      constexpr int f = decltype(F)::value;
+      for (uint32_t t = t0; t < t1 && e == cudaSuccess; ++t) {
+        k_wave32<f><<<h->f32_grid, kSyncThreads, h->P.d * sizeof(float), h->stream>>>(h->P, h->Q, h->S32, h->C,
+                                                                                      h->spec32_ctl, t);
+        e = cudaGetLastError();
+      }
+    });
+    CK(e);
+    return CUPSO_OK;
+  }
+  SpecCtl& c = *h->spec_host;
+  c = SpecCtl{t0, 1u, 0u, 1u, ~0u, 0u, 0u, 0u};
+  CK(cudaMemcpyAsync(&h->spec32_ctl->ctl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemsetAsync(&h->spec32_ctl->key, 0, sizeof(unsigned long long), h->stream));
+  const uint32_t kmax = h->spec_kmax;
+  KState32 s0 = h->S32, s1 = h->S32_alt;
+  unsigned char* rec = h->spec_rec_local;
+  void* args[] = {&h->P, &h->Q, &s0, &s1, &h->C, &h->spec32_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec};
+  for (;;) {
+    uint32_t n = 0, t = c.t0, K = c.K, ks = c.kspec;
+    while (t < t1) {
+      t += K;
+      ++n;
+      if (K >= ks) ks = std::min(2 * ks, kmax);
+      K = std::min(ks, t1 - t);
+    }
+    for (uint32_t i = 0; i < n; ++i)
+      CK(cudaLaunchKernel(h->f32_kfn, dim3(h->f32_grid), dim3(kSyncThreads), args, 0, h->stream));
+    h->spec_launches += n;
+    CK(cudaMemcpyAsync(&c, &h->spec32_ctl->ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (c.t0 >= t1) break;
+  }
+  h->spec_passes += c.passes;
+  h->spec_fails += c.fails;
+  if (c.parity) std::swap(h->S32, h->S32_alt);
+  return CUPSO_OK;
+}
+
 cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* seconds) {
   if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
   if (variant < 0 || variant >= kNumVar) return fail(CUPSO_EINVAL, "unknown variant %d", variant);
@@ -910,6 +1040,33 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
     return fail(CUPSO_EINVAL, "sharded swarms step with cuda-sync only");
   CK(cudaSetDevice(h->device));
   const uint32_t t0 = h->t, t1 = h->t + iters;
+  if (variant == CUPSO_SYNC_F32) {
+    if (h->comm) return fail(CUPSO_EINVAL, "cuda-sync-f32: sharded swarms step with cuda-sync only");
+    TRY(ensure_f32(h));
+    if (!h->spec_host) {
+      void* host = nullptr;
+      CK(cudaMallocHost(&host, sizeof(SpecCtl)));
+      h->spec_host = static_cast<SpecCtl*>(host);
+    }
+    if (!h->f32_active && iters) {  // FP64 state -> FP32 copy (outside the timed region)
+      k_to_f32<<<conv_blocks(h), 256, 0, h->stream>>>(h->P, h->S, h->S32);
+      CK(cudaGetLastError());
+      h->f32_active = true;
+    }
+    CK(cudaMemsetAsync(&h->spec32_ctl->key, 0, sizeof(unsigned long long), h->stream));
+    CK(cudaEventRecord(h->ev0, h->stream));
+    if (iters) TRY(f32_steps(h, t0, t1));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaEventSynchronize(h->ev1));
+    CK(cudaGetLastError());
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (seconds) *seconds = ms * 1e-3;
+    for (uint32_t t = t0; t < t1; ++t) h->is_async[t] = 0;
+    h->t = t1;
+    return CUPSO_OK;
+  }
+  TRY(sync_f64(h));
   cudaGraphExec_t ge = nullptr;
   if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
   // probe outside the timed region (allocates the second state buffer once)
@@ -1059,6 +1216,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
 
 cupso_status init_impl(cupso_swarm* h) {
   CK(cudaSetDevice(h->device));
+  h->f32_active = false;  // a fresh FP64 swarm
   const int blocks = static_cast<int>(std::min<uint64_t>((h->P.ld + 255) / 256, 148ull * 16));
   cudaError_t e = cudaSuccess;
   dispatch_fit(h->fid, [&](auto F) {
@@ -1098,6 +1256,7 @@ cupso_status init_impl(cupso_swarm* h) {
 cupso_status download_impl(cupso_swarm* h, double* positions, double* velocities, double* fitness,
                            double* pbest_pos, double* pbest_fit) {
   CK(cudaSetDevice(h->device));
+  TRY(sync_f64(h));
   const size_t n = h->P.n, d = h->P.d, ld = h->P.ld;
   auto rows = [&](double* dst, const double* src, size_t nrows) -> cupso_status {
     if (!dst) return CUPSO_OK;
@@ -1217,7 +1376,7 @@ int cupso_variant_id(const char* name) {
 
 const char* cupso_variant_name(int v) { return (v >= 0 && v < kNumVar) ? kVarNames[v] : nullptr; }
 int cupso_variant_count(void) { return kNumVar; }
-int cupso_variant_deterministic(int v) { return v >= 0 && v < CUPSO_ASYNC; }
+int cupso_variant_deterministic(int v) { return v >= 0 && v < CUPSO_ASYNC; }  // FP32 is statistical
 
 cupso_status cupso_validate_params(const cupso_params* p) { return validate(p); }
 
@@ -1325,6 +1484,7 @@ cupso_status cupso_upload_state(cupso_swarm* h, uint32_t iteration, const double
   if (iteration > h->T) return fail(CUPSO_EINVAL, "iteration %u beyond max_iter %u", iteration, h->T);
   CK(cudaSetDevice(h->device));
   const size_t n = h->P.n, d = h->P.d, ld = h->P.ld;
+  h->f32_active = false;  // the uploaded FP64 state is authoritative
   // neutral padding, then the rows
   if (!h->initialized) TRY(init_impl(h));
   auto rows = [&](double* dst, const double* src, size_t nrows) -> cupso_status {
@@ -1350,6 +1510,8 @@ cupso_status cupso_upload_state(cupso_swarm* h, uint32_t iteration, const double
 cupso_status cupso_device_state(cupso_swarm* h, double** pos, double** vel, double** pbest_pos,
                                 double** pbest_fit, uint64_t* ld) {
   if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
+  TRY(sync_f64(h));
+  CK(cudaStreamSynchronize(h->stream));
   if (pos) *pos = h->S.pos;
   if (vel) *vel = h->S.vel;
   if (pbest_pos) *pbest_pos = h->S.pb;
@@ -1400,6 +1562,7 @@ cupso_status cupso_shard_propose_device(cupso_swarm* h, void* record_dev) {
   if (!h->initialized) return fail(CUPSO_ELOGIC, "propose before cupso_init");
   if (h->t >= h->T) return fail(CUPSO_EINVAL, "swarm already ran max_iter (%u) iterations", h->T);
   CK(cudaSetDevice(h->device));
+  TRY(sync_f64(h));
   return propose_launch(h, h->t, static_cast<unsigned char*>(record_dev));
 }
 

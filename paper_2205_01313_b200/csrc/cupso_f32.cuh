@@ -1,0 +1,409 @@
+// cupso_f32.cuh -- the FP32 engine "cuda-sync-f32".
+//
+// The reference is FP64 throughout (swarm.hpp:31-35); this engine
+// is the north star's FP32 shape of the same synchronous algorithm, checked
+// statistically rather than bitwise:
+//   * state as FP32 SoA rows, 4 adjacent particles per thread moved with one
+//     float4 (LDG.128 / STG.128) per row;
+//   * one Philox-4x32-10 call per (t, particle, axis) -- words 0 and 1 give
+//     r1 and r2 as 24-bit uniforms (the FP64 engines draw two calls, slots 0/1);
+//   * kinematics with FMA and FMNMX clamps, fitness in FP32;
+//   * the gbest aggregation is the paper's atomic scheme on a packed 64-bit
+//     key: (order-preserving FP32 fitness << 32) | ~particle, so one u64
+//     atomicMax is "fitness descending, ties to the lower index" (beats(),
+//     engine.hpp:38-41) -- warp shuffle max, one SMEM atomicMax per warp into
+//     the block's slot, one global atomicMax per block;
+//   * the speculative register-resident passes of k_spec (cupso_spec.cuh),
+//     same SpecCtl schedule and spec_decide.
+// The handle keeps the FP64 state authoritative for every other entry point:
+// it is converted to FP32 when a cuda-sync-f32 step starts and back when any
+// FP64 consumer (another engine, download, device pointers) needs it.
+#pragma once
+
+#include "cupso_spec.cuh"
+
+namespace cupso {
+
+struct KState32 {
+  float* pos;
+  float* vel;
+  float* pb;
+  float* pbf;
+};
+
+// Run parameters in FP32 (rounded from the FP64 pso_params on the host).
+struct KParams32 {
+  float w, c1, c2, min_pos, max_pos, min_v, max_v;
+};
+
+template <int F>
+struct Fit32;
+template <>
+struct Fit32<kCubic> {
+  float acc = 0.f;
+  __device__ __forceinline__ void add(float v, uint32_t) {
+    acc += __fmaf_rn(__fmaf_rn(v - 0.8f, v, -1000.f), v, 8000.f);
+  }
+  __device__ __forceinline__ float value() const { return acc; }
+};
+template <>
+struct Fit32<kSphere> {
+  float acc = 0.f;
+  __device__ __forceinline__ void add(float v, uint32_t) { acc = __fmaf_rn(v, v, acc); }
+  __device__ __forceinline__ float value() const { return -acc; }
+};
+template <>
+struct Fit32<kRosenbrock> {
+  float acc = 0.f, prev = 0.f;
+  __device__ __forceinline__ void add(float v, uint32_t axis) {
+    if (axis > 0) {
+      const float a = __fmaf_rn(-prev, prev, v);
+      const float b = 1.f - prev;
+      acc += __fmaf_rn(100.f * a, a, b * b);
+    }
+    prev = v;
+  }
+  __device__ __forceinline__ float value() const { return -acc; }
+};
+template <>
+struct Fit32<kGriewank> {
+  float sum = 0.f, prod = 1.f;
+  __device__ __forceinline__ void add(float v, uint32_t axis) {
+    sum = __fmaf_rn(v * v, 1.f / 4000.f, sum);
+    prod *= cosf(v * rsqrtf(static_cast<float>(axis + 1)));
+  }
+  __device__ __forceinline__ float value() const { return -((1.f + sum) - prod); }
+};
+template <>
+struct Fit32<kRastrigin> {
+  float acc = 0.f;
+  __device__ __forceinline__ void add(float v, uint32_t) {
+    acc += __fmaf_rn(v, v, __fmaf_rn(-10.f, cospif(2.f * v), 10.f));
+  }
+  __device__ __forceinline__ float value() const { return -acc; }
+};
+
+// Packed (fitness, particle) key: u64 max == beats() order.
+__device__ __forceinline__ unsigned long long key32(float f, uint32_t i) {
+  const uint32_t b = __float_as_uint(f);
+  const uint32_t o = (b >> 31) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(o) << 32) | static_cast<unsigned long long>(~i);
+}
+__device__ __forceinline__ float key_fit(unsigned long long k) {
+  const uint32_t o = static_cast<uint32_t>(k >> 32);
+  return __uint_as_float((o >> 31) ? (o & 0x7fffffffu) : ~o);
+}
+__device__ __forceinline__ uint32_t key_idx(unsigned long long k) { return ~static_cast<uint32_t>(k); }
+
+template <int NP>
+__device__ __forceinline__ void ldv32(const float* p, float (&o)[NP]) {
+  if constexpr (NP == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+    o[2] = t.z;
+    o[3] = t.w;
+  } else if constexpr (NP == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = *p;
+  }
+}
+template <int NP>
+__device__ __forceinline__ void stv32(float* p, const float (&o)[NP]) {
+  if constexpr (NP == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  } else if constexpr (NP == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
+  } else {
+    *p = o[0];
+  }
+}
+
+// One Philox call -> (r1, r2), 24-bit uniforms in [0, 1).
+__device__ __forceinline__ void uniform2_f32(const KParams& P, uint32_t t, uint32_t i, uint32_t axis, float& r1,
+                                             float& r2) {
+  uint32_t c0 = t, c1 = i, c2 = axis, c3 = 0;
+  philox10(c0, c1, c2, c3, P);
+  r1 = __uint2float_rz(c0 >> 8) * 0x1.0p-24f;
+  r2 = __uint2float_rz(c1 >> 8) * 0x1.0p-24f;
+}
+
+// The key slot of the pass lives right after SpecCtl in the control buffer.
+struct SpecCtl32 {
+  SpecCtl ctl;
+  unsigned long long key;  // best (fit, particle) admitted at the pass's last iteration
+};
+
+template <int F, int D, int NP, int MINB>
+__global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParams32 Q, KState32 S0, KState32 S1,
+                                                              KCtl C, SpecCtl32* sc32, uint32_t t_end, uint32_t kmax,
+                                                              unsigned char* rec_out) {
+  __shared__ float s_gpos[D];
+  __shared__ unsigned long long s_key;
+  __shared__ unsigned long long s_adm;
+  __shared__ uint32_t s_ctl[4];
+  __shared__ int s_last;
+  SpecCtl* sc = &sc32->ctl;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    s_ctl[0] = ld_volatile_u32(&sc->t0);
+    s_ctl[1] = ld_volatile_u32(&sc->K);
+    s_ctl[2] = ld_volatile_u32(&sc->parity);
+    s_ctl[3] = ld_volatile_u32(&sc->kspec);
+    s_key = 0;
+    s_adm = 0;
+  }
+  if (tid < D) s_gpos[tid] = static_cast<float>(C.snap_pos[tid]);
+  __syncthreads();
+  const uint32_t t0 = s_ctl[0], K = s_ctl[1], par = s_ctl[2];
+  if (t0 >= t_end) return;
+  const bool inplace = K == 1;
+  const KState32 Si = par ? S1 : S0;
+  const KState32 So = inplace ? Si : (par ? S0 : S1);
+  // the FP32 engine filters against the FP32 value of the snapshot fitness
+  const float snap_fit = static_cast<float>(C.snap->fit);
+  const uint32_t tl = t0 + K - 1;
+  float gp[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) gp[a] = s_gpos[a];
+  unsigned long long bkey = 0;
+  uint32_t adm = 0;
+  uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
+  const uint32_t units = (P.n + NP - 1) / NP;
+  const size_t ld = P.ld;
+  for (uint32_t u = blockIdx.x * blockDim.x + tid; u < units; u += gridDim.x * blockDim.x) {
+    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+    uint32_t te = min(t0 + K, tstop);
+    if (te <= t0) break;
+    const uint32_t li = NP * u, g0 = P.base + li;
+    float x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
+    bool ok[NP];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const size_t at = static_cast<size_t>(a) * ld + li;
+      ldv32<NP>(Si.pos + at, x[a]);
+      ldv32<NP>(Si.vel + at, v[a]);
+      ldv32<NP>(Si.pb + at, pb[a]);
+    }
+    ldv32<NP>(Si.pbf + li, pbf);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
+    uint32_t t = t0;
+    bool bad = false, dirty = false;
+    for (; t < te; ++t) {
+      Fit32<F> acc[NP];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          float r1, r2;
+          uniform2_f32(P, t, g0 + k, a, r1, r2);
+          const float xv = x[a][k];
+          float nv = __fmaf_rn(Q.c2 * r2, gp[a] - xv, __fmaf_rn(Q.c1 * r1, pb[a][k] - xv, Q.w * v[a][k]));
+          nv = fminf(fmaxf(nv, Q.min_v), Q.max_v);
+          const float nx = fminf(fmaxf(xv + nv, Q.min_pos), Q.max_pos);
+          v[a][k] = nv;
+          x[a][k] = nx;
+          acc[k].add(nx, a);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const float f = acc[k].value();
+        if (!ok[k]) continue;
+        if (f > pbf[k]) {
+          dirty = true;
+          pbf[k] = f;
+#pragma unroll
+          for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+        }
+        if (f > snap_fit) {
+          if (t < tl) {
+            bad = true;
+          } else {
+            ++adm;
+            const unsigned long long kk = key32(f, g0 + k);
+            bkey = kk > bkey ? kk : bkey;
+          }
+        }
+      }
+      if (bad) {
+        atomicMin(&sc->tmin, t);
+        tstop = t;
+        break;
+      }
+      if (((t - t0) & 15u) == 15u) {
+        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+        te = min(te, tstop);
+      }
+    }
+    if (!bad && t == t0 + K) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const size_t at = static_cast<size_t>(a) * ld + li;
+        stv32<NP>(So.pos + at, x[a]);
+        stv32<NP>(So.vel + at, v[a]);
+      }
+      if (!inplace || dirty) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) stv32<NP>(So.pb + static_cast<size_t>(a) * ld + li, pb[a]);
+        stv32<NP>(So.pbf + li, pbf);
+      }
+    }
+  }
+  // ---- aggregation: warp shuffle max of the packed key, one SMEM atomicMax
+  // per warp, one global atomicMax per block (the paper's atomic scheme)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, bkey, off);
+    bkey = o > bkey ? o : bkey;
+  }
+  const uint32_t wadm = __reduce_add_sync(0xffffffffu, adm);
+  if (lane == 0) {
+    if (bkey) atomicMax(&s_key, bkey);
+    if (wadm) atomicAdd(&s_adm, static_cast<unsigned long long>(wadm));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (s_key) atomicMax(&sc32->key, s_key);
+    if (s_adm) atomicAdd(&C.admitted[tl], s_adm);
+    __threadfence();
+    s_last = last_block_done(C);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last block: the pass record, then the shared decision (spec_decide)
+  __threadfence();
+  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(&sc32->key);
+  SpecRec* rec = reinterpret_cast<SpecRec*>(rec_out);
+  double* rpos = reinterpret_cast<double*>(rec_out + sizeof(SpecRec));
+  const uint32_t wi = key ? key_idx(key) : kNoParticle;
+  for (uint32_t a = tid; a < D; a += blockDim.x)
+    rpos[a] = key ? static_cast<double>(__ldcg(&So.pos[static_cast<size_t>(a) * ld + (wi - P.base)])) : 0.0;
+  if (tid == 0) {
+    rec->tmin = ld_volatile_u32(&sc->tmin);
+    rec->admitted = static_cast<uint32_t>(__ldcg(&C.admitted[tl]));
+    rec->fit = key ? static_cast<double>(key_fit(key)) : -INFINITY;
+    rec->particle = wi;
+    rec->pad = 0;
+    C.admitted[tl] = 0;
+    sc32->key = 0;
+    __threadfence();
+  }
+  __syncthreads();
+  spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
+}
+
+// Any dims: one launch per iteration, one particle per thread, state in HBM
+// (the dims without a register-resident k_spec32 instantiation). Same RNG,
+// arithmetic and packed-key aggregation; the last block adopts the winner.
+template <int F>
+__global__ void __launch_bounds__(kSyncThreads) k_wave32(KParams P, KParams32 Q, KState32 S, KCtl C,
+                                                         SpecCtl32* sc32, uint32_t t) {
+  __shared__ unsigned long long s_key, s_adm;
+  __shared__ int s_last;
+  extern __shared__ float s_g[];  // [d] snapshot position
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    s_key = 0;
+    s_adm = 0;
+  }
+  for (uint32_t a = tid; a < P.d; a += blockDim.x) s_g[a] = static_cast<float>(C.snap_pos[a]);
+  __syncthreads();
+  const float snap_fit = static_cast<float>(C.snap->fit);
+  const size_t ld = P.ld;
+  unsigned long long bkey = 0;
+  uint32_t adm = 0;
+  for (uint32_t li = blockIdx.x * blockDim.x + tid; li < P.n; li += gridDim.x * blockDim.x) {
+    const uint32_t gi = P.base + li;
+    Fit32<F> acc;
+    for (uint32_t a = 0; a < P.d; ++a) {
+      const size_t at = static_cast<size_t>(a) * ld + li;
+      float r1, r2;
+      uniform2_f32(P, t, gi, a, r1, r2);
+      const float xv = S.pos[at];
+      float nv = __fmaf_rn(Q.c2 * r2, s_g[a] - xv, __fmaf_rn(Q.c1 * r1, S.pb[at] - xv, Q.w * S.vel[at]));
+      nv = fminf(fmaxf(nv, Q.min_v), Q.max_v);
+      const float nx = fminf(fmaxf(xv + nv, Q.min_pos), Q.max_pos);
+      S.vel[at] = nv;
+      S.pos[at] = nx;
+      acc.add(nx, a);
+    }
+    const float f = acc.value();
+    if (f > S.pbf[li]) {
+      S.pbf[li] = f;
+      for (uint32_t a = 0; a < P.d; ++a) {
+        const size_t at = static_cast<size_t>(a) * ld + li;
+        S.pb[at] = S.pos[at];
+      }
+    }
+    if (f > snap_fit) {
+      ++adm;
+      const unsigned long long kk = key32(f, gi);
+      bkey = kk > bkey ? kk : bkey;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, bkey, off);
+    bkey = o > bkey ? o : bkey;
+  }
+  const uint32_t wadm = __reduce_add_sync(0xffffffffu, adm);
+  if (lane == 0) {
+    if (bkey) atomicMax(&s_key, bkey);
+    if (wadm) atomicAdd(&s_adm, static_cast<unsigned long long>(wadm));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (s_key) atomicMax(&sc32->key, s_key);
+    if (s_adm) atomicAdd(&C.admitted[t], s_adm);
+    __threadfence();
+    s_last = last_block_done(C);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(&sc32->key);
+  if (key) {
+    const uint32_t wi = key_idx(key);
+    for (uint32_t a = tid; a < P.d; a += blockDim.x)
+      C.snap_pos[a] = static_cast<double>(__ldcg(&S.pos[static_cast<size_t>(a) * ld + (wi - P.base)]));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (key) {  // every admitted key beat the snapshot: adopt the max
+      C.snap->fit = static_cast<double>(key_fit(key));
+      C.snap->particle = key_idx(key);
+    }
+    C.trace[t] = C.snap->fit;
+    C.trace_idx[t] = C.snap->particle;
+    sc32->key = 0;
+  }
+}
+
+// FP64 <-> FP32 state conversion (rows of ld, all 3d+1 arrays).
+__global__ void k_to_f32(KParams P, KState S, KState32 T) {
+  const size_t cells = static_cast<size_t>(P.d) * P.ld;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    T.pos[i] = static_cast<float>(S.pos[i]);
+    T.vel[i] = static_cast<float>(S.vel[i]);
+    T.pb[i] = static_cast<float>(S.pb[i]);
+    if (i < P.ld) T.pbf[i] = static_cast<float>(S.pbf[i]);
+  }
+}
+__global__ void k_to_f64(KParams P, KState32 T, KState S) {
+  const size_t cells = static_cast<size_t>(P.d) * P.ld;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    S.pos[i] = T.pos[i];
+    S.vel[i] = T.vel[i];
+    S.pb[i] = T.pb[i];
+    if (i < P.ld) S.pbf[i] = T.pbf[i];
+  }
+}
+
+}  // namespace cupso

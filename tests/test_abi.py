@@ -54,9 +54,9 @@ def test_abi_version_and_registry(cupso):
     assert boxes["griewank"] == (-600.0, 600.0) and boxes["rastrigin"] == (-5.12, 5.12)
     engines = cupso.engine_registry()
     assert [e.name for e in engines] == ["cuda-reduction", "cuda-unrolled", "cuda-queue",
-                                         "cuda-queue-lock", "cuda-sync", "cuda-async"]
+                                         "cuda-queue-lock", "cuda-sync", "cuda-async", "cuda-sync-f32"]
     assert all(e.parallel for e in engines)
-    assert [e.deterministic for e in engines] == [True] * 5 + [False]
+    assert [e.deterministic for e in engines] == [True] * 5 + [False, False]
     assert cupso.find_engine("sync").name == "cuda-sync"  # short names accepted
 
 

@@ -1,0 +1,71 @@
+"""GPU: the FP32 engine cuda-sync-f32.
+
+FP32 state with float4 rows, one Philox call per particle-axis, FMA
+kinematics, and the paper's packed 64-bit (fitness, index) atomicMax
+aggregation. Not bitwise against the FP64 reference: checked statistically
+(final fitness over 32 seeds against cuda-sync) and by invariants.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_f32_statistics_32_seeds(cupso):
+    f = cupso.find_fitness("sphere")
+    p = cupso.make_params(f, 4096, 4, 300)
+    sync = np.array([cupso.find_engine("cuda-sync").run(p, f, cupso.rng_key(s)).gbest_fit for s in range(1, 33)])
+    f32 = np.array([cupso.find_engine("cuda-sync-f32").run(p, f, cupso.rng_key(s)).gbest_fit for s in range(1, 33)])
+    assert (f32 <= 0).all()
+    med_s, med_f = np.median(-sync), np.median(-f32)
+    assert med_f < 10 * med_s + 1e-3, (med_f, med_s)
+    assert med_f < 1.0
+
+
+@pytest.mark.parametrize("fit,d", [("cubic", 1), ("sphere", 8), ("rastrigin", 2), ("rosenbrock", 4),
+                                   ("griewank", 3), ("sphere", 5)])
+def test_f32_invariants(cupso, oracle, fit, d):
+    """Monotone trace; the record is a consistent (fit, pos) pair of an FP32
+    particle; gbest = max pbest; state in the box. d = 3 / 5 run k_wave32."""
+    f = cupso.find_fitness(fit)
+    n, T = 5001, 90
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, 7) as sw:
+        sw.step(cupso.SYNC_F32, 40)
+        sw.step(cupso.SYNC_F32, T - 40)
+        tr, tp, occ = sw.trace()
+        gb = sw.gbest()
+        st = sw.state()
+        init_fit = sw.initial_gbest()[0]
+    assert (np.diff(tr) >= 0).all() and tr[0] >= init_fit
+    assert tr[-1] == gb.fit and tp[-1] == gb.particle
+    assert gb.fit == st.pbest_fit.max()
+    holder = gb.particle
+    pb = st.pbest_pos.reshape(d, n)[:, holder]
+    assert np.array_equal(pb.astype(np.float32).astype(np.float64), pb)  # an FP32 state
+    assert np.array_equal(pb, gb.pos)
+    assert abs(oracle.fitness(fit, gb.pos) - gb.fit) <= 1e-4 * max(1.0, abs(gb.fit))
+    assert (np.abs(st.positions) <= np.float32(f.hi)).all()  # the FP32 box (bounds rounded to FP32)
+    assert ((occ >= 0) & (occ <= 1)).all()
+
+
+def test_f32_cfg2_shape_converges(cupso):
+    f = cupso.find_fitness("cubic")
+    p = cupso.make_params(f, 1 << 20, 1, 200)
+    r = cupso.find_engine("cuda-sync-f32").run(p, f, cupso.rng_key(1))
+    assert r.gbest_fit == 900000.0 and len(r.trace) == 200
+
+
+def test_f32_then_fp64_engines(cupso):
+    """Switching engines converts the state (FP32 -> FP64) transparently."""
+    f = cupso.find_fitness("sphere")
+    p = cupso.make_params(f, 3000, 8, 60)
+    with cupso.Swarm(p, f, 3) as sw:
+        sw.step(cupso.SYNC_F32, 20)
+        sw.step(cupso.SYNC, 20)
+        sw.step(cupso.SYNC_F32, 10)
+        sw.step(cupso.QUEUE_LOCK, 10)
+        tr, _, _ = sw.trace()
+        st = sw.state()
+        gb = sw.gbest()
+    assert (np.diff(tr) >= 0).all() and gb.fit == st.pbest_fit.max()
