@@ -174,8 +174,8 @@ __device__ __forceinline__ void spec_finish(const KParams& P, const KState& So, 
         C.q_fit[slot] = f;
         C.q_idx[slot] = i;
       }
-      for (uint32_t a = lane; a < D; a += 32)
-        C.q_pos[static_cast<size_t>(slot) * D + a] = So.pos[static_cast<size_t>(a) * ld + (i - P.base)];
+      for (uint32_t a = lane; a < P.d; a += 32)
+        C.q_pos[static_cast<size_t>(slot) * P.d + a] = So.pos[static_cast<size_t>(a) * ld + (i - P.base)];
     }
     __threadfence();
     __syncwarp();
@@ -194,8 +194,8 @@ __device__ __forceinline__ void spec_finish(const KParams& P, const KState& So, 
   if (nq) resolve_queue(C, 0, nq, rs, wf, wi, ws);
   SpecRec* rec = reinterpret_cast<SpecRec*>(rec_out);
   double* rpos = reinterpret_cast<double*>(rec_out + sizeof(SpecRec));
-  for (uint32_t a = tid; a < D; a += blockDim.x)
-    rpos[a] = nq ? __ldcg(&C.q_pos[static_cast<size_t>(ws) * D + a]) : 0.0;
+  for (uint32_t a = tid; a < P.d; a += blockDim.x)
+    rpos[a] = nq ? __ldcg(&C.q_pos[static_cast<size_t>(ws) * P.d + a]) : 0.0;
   if (tid == 0) {
     rec->tmin = ld_volatile_u32(&sc->tmin);
     rec->admitted = static_cast<uint32_t>(__ldcg(&C.admitted[tl]));
@@ -348,11 +348,14 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
 // of registers -- fewer live registers, so more resident warps and no spills
 // for the cos-heavy fitnesses; dynamic SMEM = (3 + term width) * DL * blockDim
 // doubles.
-template <int F, int DL, int G, int MINB, bool SM = false>
+// RAGGED: the swarm's d is below DL * G (any d up to 256): lane s holds the
+// valid axes of [s*DL, s*DL + DL) and skips the rest (warp-uniform tests).
+template <int F, int DL, int G, int MINB, bool SM = false, bool RAGGED = false>
 __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KState S0, KState S1, KCtl C,
                                                                   SpecCtl* sc, uint32_t t_end, uint32_t kmax,
                                                                   unsigned char* rec_out, int sharded) {
   constexpr int D = DL * G;
+  static_assert(!(SM && RAGGED), "the SMEM-state split kernel needs d == DL * G");
   extern __shared__ double s_state[];
   static_assert(32 % G == 0, "G must divide the warp");
   __shared__ double s_gpos[D];
@@ -370,11 +373,12 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
     bc.n = 0;
     bc.adm = 0;
   }
-  for (uint32_t a = tid; a < D; a += blockDim.x) s_gpos[a] = C.snap_pos[a];
+  for (uint32_t a = tid; a < D; a += blockDim.x) s_gpos[a] = a < P.d ? C.snap_pos[a] : 0.0;
   __syncthreads();
   const uint32_t t0 = s_ctl[0], K = s_ctl[1], par = s_ctl[2];
   if (t0 >= t_end) return;
   const bool inplace = K == 1;
+  auto valid = [&](int a) { return !RAGGED || sub * DL + a < P.d; };
   const KState Si = par ? S1 : S0;
   const KState So = inplace ? Si : (par ? S0 : S1);
   const double snap_fit = C.snap->fit;
@@ -411,6 +415,10 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
     if (live) {
 #pragma unroll
       for (int a = 0; a < DL; ++a) {
+        if (!valid(a)) {
+          X(a) = V(a) = PB(a) = 0.0;
+          continue;
+        }
         const size_t at = static_cast<size_t>(a0 + a) * ld + li;
         X(a) = Si.pos[at];
         V(a) = Si.vel[at];
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
         double xs[F == kRosenbrock ? DL : 1];  // rosenbrock's fold needs the positions
 #pragma unroll
         for (int a = 0; a < DL; ++a) {
+          if (!valid(a)) continue;  // ragged tail: warp-uniform per lane group
           const double r1 = uniform01(P, t, gi, a0 + a, 0);
           const double r2 = uniform01(P, t, gi, a0 + a, 1);
           const double x0 = X(a);
@@ -485,7 +494,8 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
           if (q > 0) acc.shfl_up(0xffffffffu, G);
           if (sub == static_cast<uint32_t>(q)) {
 #pragma unroll
-            for (int a = 0; a < DL; ++a) acc.accum(tm[a], F == kRosenbrock ? xs[a] : 0.0, a0 + a);
+            for (int a = 0; a < DL; ++a)
+              if (valid(a)) acc.accum(tm[a], F == kRosenbrock ? xs[a] : 0.0, a0 + a);
           }
         }
       }
@@ -522,6 +532,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
     if (!bad && t == t0 + K && live) {
 #pragma unroll
       for (int a = 0; a < DL; ++a) {
+        if (!valid(a)) continue;
         const size_t at = static_cast<size_t>(a0 + a) * ld + li;
         So.pos[at] = X(a);
         So.vel[at] = V(a);

@@ -43,7 +43,7 @@ def compare_state(got, orc, fit, what):
             assert_close(getattr(got, k), orc.state[k], f"{what} {k}")
 
 
-@pytest.mark.parametrize("d", [1, 2, 4, 8, 16, 32, 64])
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 8, 12, 16, 32, 64, 120])
 @pytest.mark.parametrize("fit", FITNESS)
 def test_spec_matches_oracle(cupso, oracle, spec_env, fit, d):
     n, T, seed = 3001, 120, 11  # odd n: the last two-particle unit is half padding
@@ -143,7 +143,7 @@ def test_spec_single_particle_and_single_iteration(cupso, oracle, spec_env):
         compare_state(got["state"], orc, "sphere", f"n={n} T={T}")
 
 
-@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7"])
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7", "8"])
 def test_spec_split_tunings_agree(cupso, oracle, monkeypatch, cfg):
     """d = 32 (the cfg4 shape): every lanes-per-particle split of k_spec_split is bit-identical."""
     monkeypatch.setenv("CUPSO_SYNC_MODE", "spec")
@@ -181,3 +181,16 @@ def test_spec_cfg5_shape_equals_wave(cupso, monkeypatch):
     assert_bitwise(a[3], b[3], "positions (strided sample)")
     assert_bitwise(a[4], b[4], "pbest_fit")
     assert a[5][0] < T  # temporally blocked: fewer passes than iterations
+
+
+@pytest.mark.parametrize("n", [1000, 1 << 16, 1 << 19 + 1])
+def test_spec_d1_unit_policy(cupso, oracle, spec_env, n):
+    """d = 1: small swarms take one particle per thread, large ones four (float-free
+    double2 pairs); every choice stays bit-identical to the oracle."""
+    T = 40
+    got = run_sync(cupso, "sphere", n, 1, T, 13)
+    orc = oracle.run_serial("sphere", n, 1, T, 13, want_state=n < 100000)
+    assert_bitwise(got["trace"], orc.trace, f"n={n}")
+    assert np.array_equal(got["trace_particle"], orc.trace_particle)
+    if n < 100000:
+        compare_state(got["state"], orc, "sphere", f"n={n}")

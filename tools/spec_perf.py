@@ -15,7 +15,8 @@ with cp.Swarm(p, f, 1) as sw:
                           gbs=n * T / best * (5 * d + 1) * 8 / 1e9, stats=sw.spec_stats(), gbest=sw.gbest().fit)))
 ''' % ROOT
 shapes = [("cubic", 1 << 20, 1, 1000), ("cubic", 1 << 24, 1, 100), ("sphere", 1 << 24, 8, 50), ("sphere", 1 << 26, 8, 50),
-          ("rastrigin", 1 << 20, 8, 200), ("sphere", 1 << 20, 2, 500), ("rastrigin", 1 << 20, 32, 300)]
+          ("rastrigin", 1 << 20, 8, 200), ("sphere", 1 << 20, 2, 500), ("rastrigin", 1 << 20, 32, 300),
+          ("cubic", 2048, 1, 100000), ("cubic", 65536, 1, 10000), ("cubic", 32768, 120, 1000), ("cubic", 1024, 1, 1000)]
 modes = sys.argv[1].split(",") if len(sys.argv) > 1 else ["spec", "resident", "wave"]
 if len(sys.argv) > 2:  # shape filter: indices into `shapes`
     shapes = [shapes[int(i)] for i in sys.argv[2].split(",")]
