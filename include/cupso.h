@@ -187,6 +187,17 @@ cupso_status cupso_shard_propose(cupso_swarm* h, void* record_host);
 cupso_status cupso_shard_propose_device(cupso_swarm* h, void* record_dev);  /* stays on stream */
 cupso_status cupso_shard_commit(cupso_swarm* h, const void* records_host, uint32_t nrecords);
 cupso_status cupso_shard_commit_device(cupso_swarm* h, const void* records_dev, uint32_t nrecords);
+/* Host-driven exchange (any transport: MPI, sockets, threads): like a
+ * cupso_step(h, CUPSO_SYNC, iters) of an NCCL-initialised shard, but every
+ * exchange calls fn(local, all, bytes, user), which must all-gather `bytes`
+ * from each of the nranks shards into `all` in rank order and return 0. The
+ * record is a speculative pass's SpecRec when the shard runs speculative passes,
+ * else the per-iteration candidate record. Every shard of the swarm must call
+ * it with the same iters. */
+typedef int (*cupso_exchange_fn)(const void* local, void* all, size_t bytes, void* user);
+cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks, cupso_exchange_fn fn,
+                                 void* user, double* device_seconds);
+
 /* NCCL-backed exchange: after cupso_nccl_init every cupso_step(h, CUPSO_SYNC, k)
  * on a shard runs propose -> ncclAllGather -> commit per iteration, all on the
  * shard's stream (no host round trip). unique_id = 128-byte ncclUniqueId. */

@@ -38,6 +38,7 @@ class cupso_state_view(C.Structure):
 
 
 OBSERVER_FN = C.CFUNCTYPE(None, C.c_uint32, C.POINTER(cupso_state_view), C.c_void_p)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 class cupso_result(C.Structure):
@@ -90,6 +91,7 @@ SIGNATURES = {
     "cupso_sync_grid_blocks": (C.c_int, [_vp]),
     "cupso_sync_mode": (C.c_int, [_vp]),
     "cupso_spec_stats": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "cupso_step_exchange": (C.c_int, [_vp, C.c_uint32, C.c_uint32, EXCHANGE_FN, _vp, _dp]),
     "cupso_async_mode": (C.c_int, [_vp]),
     "cupso_record_bytes": (C.c_size_t, [C.c_uint32]),
     "cupso_shard_snapshot": (C.c_int, [_vp, _vp]),

@@ -172,6 +172,13 @@ struct cupso_swarm {
   SpecCtl* spec_host = nullptr;  // pinned mirror
   uint32_t spec_kmax = 64;
   size_t spec_smem = 0;        // dynamic SMEM of the chosen spec kernel
+  // host-driven exchange (cupso_step_exchange): the caller's all-gather
+  cupso_exchange_fn xfn = nullptr;
+  void* xuser = nullptr;
+  uint32_t xranks = 0;
+  std::vector<unsigned char> xlocal, xall;
+  unsigned char* xrec_dev = nullptr;  // [xranks] gathered records on the device
+  size_t xrec_cap = 0;
   unsigned char* spec_rec_local = nullptr;  // this shard's SpecRec of the running pass
   unsigned char* spec_rec_all = nullptr;    // [nranks] all-gathered records (sharded)
   uint64_t spec_passes = 0, spec_fails = 0, spec_launches = 0;
@@ -746,6 +753,35 @@ bool spec_fits(cupso_swarm* h) {
   return true;
 }
 
+// The all-gather of one record per shard: NCCL on the stream, or the
+// caller's host callback (cupso_step_exchange). Returns the device buffer of
+// the gathered records in *all.
+cupso_status exchange(cupso_swarm* h, const unsigned char* local_dev, size_t bytes, unsigned char** all) {
+  if (h->comm) {
+    const int r = nccl().allGather(local_dev, h->spec_rec_all, bytes, /*ncclInt8*/ 0, h->comm, h->stream);
+    if (r != 0)
+      return fail(CUPSO_ERUNTIME, "ncclAllGather failed: %s", nccl().getErrorString ? nccl().getErrorString(r) : "?");
+    *all = h->spec_rec_all;
+    return CUPSO_OK;
+  }
+  const size_t need = bytes * h->xranks;
+  if (h->xrec_cap < need) {
+    void* p;
+    TRY(dmalloc(h, &p, need));
+    h->xrec_dev = static_cast<unsigned char*>(p);
+    h->xrec_cap = need;
+  }
+  h->xlocal.resize(bytes);
+  h->xall.resize(need);
+  CK(cudaMemcpyAsync(h->xlocal.data(), local_dev, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->xfn(h->xlocal.data(), h->xall.data(), bytes, h->xuser) != 0)
+    return fail(CUPSO_ERUNTIME, "exchange callback failed");
+  CK(cudaMemcpyAsync(h->xrec_dev, h->xall.data(), need, cudaMemcpyHostToDevice, h->stream));
+  *all = h->xrec_dev;
+  return CUPSO_OK;
+}
+
 cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   SpecCtl& c = *h->spec_host;
   c = SpecCtl{t0, 1u, 0u, 1u, ~0u, 0u, 0u, 0u};
@@ -756,7 +792,8 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   const void* kfn = k.fn;
   const uint32_t kmax = h->spec_kmax;
   KState s0 = h->S, s1 = h->S_alt;
-  int sharded = h->comm != nullptr;
+  int sharded = h->comm != nullptr || h->xfn != nullptr;
+  const uint32_t nrec = h->comm ? static_cast<uint32_t>(h->nranks) : h->xranks;
   unsigned char* rec = h->spec_rec_local;
   void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec, &sharded};
   const size_t rb = spec_rec_bytes(h->P.d);
@@ -772,12 +809,9 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
     for (uint32_t i = 0; i < n; ++i) {
       CK(cudaLaunchKernel(kfn, dim3(h->spec_grid), dim3(kSyncThreads), args, h->spec_smem, h->stream));
       if (sharded) {  // one exchange per pass: the shards' records, then the same decision everywhere
-        const int r = nccl().allGather(h->spec_rec_local, h->spec_rec_all, rb, /*ncclInt8*/ 0, h->comm, h->stream);
-        if (r != 0)
-          return fail(CUPSO_ERUNTIME, "ncclAllGather (spec pass) failed: %s",
-                      nccl().getErrorString ? nccl().getErrorString(r) : "?");
-        k_spec_commit<<<1, 256, 0, h->stream>>>(h->P, h->C, h->spec_ctl, h->spec_rec_all,
-                                                 static_cast<uint32_t>(h->nranks), t1, kmax);
+        unsigned char* all = nullptr;
+        TRY(exchange(h, h->spec_rec_local, rb, &all));
+        k_spec_commit<<<1, 256, 0, h->stream>>>(h->P, h->C, h->spec_ctl, all, nrec, t1, kmax);
         CK(cudaGetLastError());
       }
     }
@@ -905,12 +939,18 @@ cupso_status sharded_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   NcclApi& api = nccl();
   for (uint32_t t = t0; t < t1; ++t) {
     TRY(propose_launch(h, t, h->rec_local));
-    const int r = api.allGather(h->rec_local, h->rec_all, h->rec_bytes, /*ncclInt8*/ 0, h->comm,
-                                h->stream);
-    if (r != 0)
-      return fail(CUPSO_ERUNTIME, "ncclAllGather failed: %s",
-                  api.getErrorString ? api.getErrorString(r) : "?");
-    TRY(commit_launch(h, t, h->rec_all, static_cast<uint32_t>(h->nranks)));
+    if (h->comm) {
+      const int r = api.allGather(h->rec_local, h->rec_all, h->rec_bytes, /*ncclInt8*/ 0, h->comm,
+                                  h->stream);
+      if (r != 0)
+        return fail(CUPSO_ERUNTIME, "ncclAllGather failed: %s",
+                    api.getErrorString ? api.getErrorString(r) : "?");
+      TRY(commit_launch(h, t, h->rec_all, static_cast<uint32_t>(h->nranks)));
+    } else {  // host callback exchange
+      unsigned char* all = nullptr;
+      TRY(exchange(h, h->rec_local, h->rec_bytes, &all));
+      TRY(commit_launch(h, t, all, h->xranks));
+    }
   }
   return CUPSO_OK;
 }
@@ -1083,7 +1123,8 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
   // probe outside the timed region (allocates the second state buffer once)
   const bool spec = iters && variant == CUPSO_SYNC && spec_fits(h);
-  const bool wave = variant == CUPSO_SYNC && h->wave && !h->comm && !spec;
+  const bool shard_x = h->comm || h->xfn;  // exchanged with other shards
+  const bool wave = variant == CUPSO_SYNC && h->wave && !shard_x && !spec;
   if (iters && wave) {
     TRY(wave_graph(h, t0, iters, &ge));
     CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
@@ -1093,7 +1134,7 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
     TRY(copy_record(h, h->C.live, h->C.snap));
     CK(cudaMemsetAsync(h->C.trace_key + t0, 0, iters * sizeof(unsigned long long), h->stream));
   }
-  if (iters && variant == CUPSO_SYNC && !wave && !spec && !h->comm) resident_fits(h);  // probe outside the timed region
+  if (iters && variant == CUPSO_SYNC && !wave && !spec && !shard_x) resident_fits(h);  // probe outside the timed region
   if (iters && variant == CUPSO_ASYNC && !async_reg_fits(h)) tiled_fits(h);
   if (iters && ((variant == CUPSO_SYNC && !wave && !spec) || variant == CUPSO_ASYNC)) TRY(ensure_sync_grid(h));
   CK(cudaEventRecord(h->ev0, h->stream));
@@ -1102,7 +1143,7 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
       CK(cudaGraphLaunch(ge, h->stream));
     } else if (spec) {
       TRY(spec_steps(h, t0, t1));
-    } else if (variant == CUPSO_SYNC && h->comm) {
+    } else if (variant == CUPSO_SYNC && (h->comm || h->xfn)) {
       TRY(sharded_steps(h, t0, t1));
     } else {
       constexpr uint32_t kChunk = 1u << 20;  // keeps the barrier counter far from wrap
@@ -1451,6 +1492,20 @@ cupso_status cupso_init(cupso_swarm* h) {
 
 cupso_status cupso_step(cupso_swarm* h, int variant, uint32_t iters, double* device_seconds) {
   return do_step(h, variant, iters, device_seconds);
+}
+
+cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks, cupso_exchange_fn fn,
+                                 void* user, double* device_seconds) {
+  if (!h || !fn) return fail(CUPSO_EINVAL, "null argument");
+  if (nranks < 1) return fail(CUPSO_EINVAL, "cupso_step_exchange: nranks must be >= 1");
+  if (h->comm) return fail(CUPSO_EINVAL, "cupso_step_exchange: the handle exchanges over NCCL");
+  h->xfn = fn;
+  h->xuser = user;
+  h->xranks = nranks;
+  const cupso_status st = do_step(h, CUPSO_SYNC, iters, device_seconds);
+  h->xfn = nullptr;
+  h->xuser = nullptr;
+  return st;
 }
 
 cupso_status cupso_synchronize(cupso_swarm* h) {

@@ -162,6 +162,31 @@ class Swarm:
         buf = C.create_string_buffer(bytes(blob), len(blob))
         check(lib().cupso_shard_commit(self._h, buf, n))
 
+    def step_exchange(self, iters: int, nranks: int, allgather) -> float:
+        """cuda-sync steps of a host-exchanged shard: allgather(local: bytes) -> list of
+        nranks records (bytes, rank order). Called once per speculative pass (or per
+        iteration where no speculative kernel exists); every shard must step alike."""
+        err = []
+
+        def cb(local, allp, nbytes, _user):
+            try:
+                recs = allgather(C.string_at(local, nbytes))
+                blob = b"".join(recs)
+                assert len(blob) == nbytes * nranks
+                C.memmove(allp, blob, len(blob))
+                return 0
+            except Exception as e:  # surfaced after the call returns
+                err.append(e)
+                return 1
+
+        fn = _lib.EXCHANGE_FN(cb)
+        s = C.c_double()
+        st = lib().cupso_step_exchange(self._h, iters, nranks, fn, None, C.byref(s))
+        if err:
+            raise err[0]
+        check(st)
+        return s.value
+
     def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib().cupso_nccl_init(self._h, buf, nranks, rank))

@@ -45,6 +45,73 @@ def test_shards_with_host_exchange_equal_single_swarm(cupso, fitness, n, d, T, s
             sh.close()
 
 
+class _ThreadAllGather:
+    """An all-gather between host threads (one per shard) for cupso_step_exchange."""
+
+    def __init__(self, n):
+        import threading
+        self.n, self.slots, self.bar = n, [None] * n, threading.Barrier(n)
+
+    def __call__(self, rank, local):
+        self.slots[rank] = local
+        self.bar.wait()
+        out = list(self.slots)
+        self.bar.wait()
+        return out
+
+
+@pytest.mark.parametrize("fitness,n,d,T,shards,mode", [("sphere", 20001, 8, 60, 2, "auto"),
+                                                        ("cubic", 65536, 1, 80, 4, "auto"),
+                                                        ("rastrigin", 3001, 32, 40, 3, "auto"),
+                                                        ("rosenbrock", 5001, 5, 50, 2, "auto"),
+                                                        ("sphere", 3001, 4, 30, 2, "wave")])
+def test_shards_step_exchange_equal_single_swarm(cupso, monkeypatch, fitness, n, d, T, shards, mode):
+    """The sharded speculative protocol on the device (k_spec with a pass record,
+    all-gather, k_spec_commit on every shard) with the all-gather done by host
+    threads: G shards on one GPU == one swarm, bitwise (trace, gbest index
+    trajectory, every shard's state). mode=wave: the per-iteration protocol."""
+    import threading
+    monkeypatch.setenv("CUPSO_SYNC_MODE", mode)
+    f = cupso.find_fitness(fitness)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, 33) as whole:
+        whole.step(cupso.SYNC, T)
+        wtr, wtp, _ = whole.trace()
+        wst = whole.state()
+    parts = [cupso.Swarm(p, f, 33, first=a, count=c, init=False)
+             for a, c in (cupso.shard_range(n, shards, r) for r in range(shards))]
+    try:
+        cupso.init_shards(parts)
+        ag = _ThreadAllGather(shards)
+        errs = []
+
+        def run(r):
+            try:
+                parts[r].step_exchange(T // 2, shards, lambda loc: ag(r, loc))
+                parts[r].step_exchange(T - T // 2, shards, lambda loc: ag(r, loc))
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(shards)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        assert not errs, errs
+        want_mode = "spec" if mode == "auto" else "wave"
+        for sh in parts:
+            tr, tp, _ = sh.trace()
+            assert same(tr, wtr) and np.array_equal(tp, wtp)
+            assert sh.sync_mode() in (want_mode, "persistent")
+        pos = np.concatenate([sh.state().positions.reshape(d, -1) for sh in parts], axis=1)
+        assert same(pos.reshape(-1), wst.positions)
+        if mode == "auto":
+            assert parts[0].spec_stats()[0] < T  # temporally blocked passes, exchanged per pass
+    finally:
+        for sh in parts:
+            sh.close()
+
+
 @pytest.mark.parametrize("mode,d,want", [("auto", 4, "nccl-sharded-spec"), ("auto", 32, "nccl-sharded-spec"),
                                          ("auto", 3, "nccl-sharded-spec"), ("wave", 4, "nccl-sharded"),
                                          ("persistent", 3, "nccl-sharded")])
