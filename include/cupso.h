@@ -195,6 +195,11 @@ cupso_status cupso_shard_commit_device(cupso_swarm* h, const void* records_dev, 
  * else the per-iteration candidate record. Every shard of the swarm must call
  * it with the same iters. */
 typedef int (*cupso_exchange_fn)(const void* local, void* all, size_t bytes, void* user);
+/* Shards of one swarm driven from one process: let a shard that falsifies a
+ * speculative pass stop the others early (each sees the others' pass-control
+ * word). An optimisation only -- results never depend on it. NCCL shards do the
+ * same through CUDA IPC at their first speculative step. */
+cupso_status cupso_shard_link(cupso_swarm** shards, uint32_t n);
 cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks, cupso_exchange_fn fn,
                                  void* user, double* device_seconds);
 

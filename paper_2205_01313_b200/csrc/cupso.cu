@@ -177,6 +177,7 @@ struct cupso_swarm {
   void* xuser = nullptr;
   uint32_t xranks = 0;
   std::vector<unsigned char> xlocal, xall;
+  std::vector<void*> ipc_opened;      // peer SpecCtl mappings (CUDA IPC)
   unsigned char* xrec_dev = nullptr;  // [xranks] gathered records on the device
   size_t xrec_cap = 0;
   unsigned char* spec_rec_local = nullptr;  // this shard's SpecRec of the running pass
@@ -700,6 +701,51 @@ SpecPick spec_kernel(uint32_t d, uint32_t n, int nsm) {
   return k;
 }
 
+// NCCL shards: map every other rank's SpecCtl (CUDA IPC over NVLink) so a
+// falsified pass stops all shards early (KCtl.peer_tmin). Every rank calls
+// this once, collectively (one all-gather of the 64-byte IPC handles); any
+// failure leaves npeers = 0 -- the hints are an optimisation, never needed
+// for the result. CUPSO_SPEC_PEERS=0 disables.
+void link_ipc_peers(cupso_swarm* h) {
+  h->C.npeers = 0;
+  const char* e = getenv("CUPSO_SPEC_PEERS");
+  const bool want = !(e && !strcmp(e, "0")) && h->nranks > 1 && h->nranks <= 16;
+  // the all-gather runs on every rank whatever it decides, so collectives stay matched
+  struct Slot {
+    cudaIpcMemHandle_t hnd;
+    int ok;
+    int pad[15];
+  };
+  Slot mine{};
+  mine.ok = want && cudaIpcGetMemHandle(&mine.hnd, h->spec_ctl) == cudaSuccess;
+  cudaGetLastError();
+  void *dsend = nullptr, *drecv = nullptr;
+  std::vector<Slot> all(h->nranks);
+  bool ok = cudaMalloc(&dsend, sizeof(Slot)) == cudaSuccess &&
+            cudaMalloc(&drecv, sizeof(Slot) * h->nranks) == cudaSuccess &&
+            cudaMemcpyAsync(dsend, &mine, sizeof(Slot), cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
+  ok = ok && nccl().allGather(dsend, drecv, sizeof(Slot), /*ncclInt8*/ 0, h->comm, h->stream) == 0;
+  ok = ok && cudaMemcpyAsync(all.data(), drecv, sizeof(Slot) * h->nranks, cudaMemcpyDeviceToHost, h->stream) ==
+                 cudaSuccess;
+  ok = ok && cudaStreamSynchronize(h->stream) == cudaSuccess;
+  if (dsend) cudaFree(dsend);
+  if (drecv) cudaFree(drecv);
+  for (int r = 0; ok && r < h->nranks; ++r) ok = all[r].ok != 0;
+  uint32_t np = 0;
+  for (int r = 0; ok && r < h->nranks; ++r) {
+    if (r == h->rank) continue;
+    void* base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, all[r].hnd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      ok = false;
+      break;
+    }
+    h->ipc_opened.push_back(base);
+    h->C.peer_tmin[np++] = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(base) + offsetof(SpecCtl, tmin));
+  }
+  cudaGetLastError();
+  h->C.npeers = ok ? np : 0;
+}
+
 bool spec_fits(cupso_swarm* h) {
   if (h->spec_checked) return h->spec_grid > 0;
   h->spec_checked = true;
@@ -750,6 +796,7 @@ bool spec_fits(cupso_swarm* h) {
   const char* ke = getenv("CUPSO_SPEC_K");
   h->spec_kmax = ke ? std::max(1, atoi(ke)) : 64;
   h->spec_grid = static_cast<int>(grid);
+  if (h->comm) link_ipc_peers(h);
   return true;
 }
 
@@ -1476,6 +1523,7 @@ cupso_status cupso_destroy(cupso_swarm* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : h->allocs) cudaFree(p);
   if (h->spec_host) cudaFreeHost(h->spec_host);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -1506,6 +1554,30 @@ cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks
   h->xfn = nullptr;
   h->xuser = nullptr;
   return st;
+}
+
+cupso_status cupso_shard_link(cupso_swarm** shards, uint32_t n) {
+  if (!shards || n < 1 || n > 16) return fail(CUPSO_EINVAL, "cupso_shard_link: 1..16 shards");
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!shards[i]) return fail(CUPSO_EINVAL, "null shard handle");
+    CK(cudaSetDevice(shards[i]->device));
+    if (!spec_fits(shards[i])) return CUPSO_OK;  // no speculative passes on this shape: nothing to link
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t np = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      if (shards[j]->device != shards[i]->device) {
+        CK(cudaSetDevice(shards[i]->device));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(shards[j]->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        cudaGetLastError();
+      }
+      shards[i]->C.peer_tmin[np++] = &shards[j]->spec_ctl->tmin;
+    }
+    shards[i]->C.npeers = np;
+  }
+  return CUPSO_OK;
 }
 
 cupso_status cupso_synchronize(cupso_swarm* h) {

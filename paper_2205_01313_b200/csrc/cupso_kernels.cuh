@@ -55,7 +55,19 @@ struct KCtl {
   uint32_t* q_idx;                // [3*cap]
   double* q_pos;                  // [3*cap*d]
   uint32_t q_cap;
+  // speculative passes of a sharded swarm: the other shards' SpecCtl.tmin
+  // words (same process, or CUDA IPC over NVLink). A shard that falsifies a
+  // pass lowers them too, so every shard stops early -- a hint only: the
+  // decision always comes from the exchanged pass records.
+  uint32_t npeers;
+  uint32_t* peer_tmin[15];
 };
+
+// Lower this shard's tmin and, when that was news, the peers' (rare path).
+__device__ __forceinline__ void spec_falsify(const KCtl& C, uint32_t* tmin, uint32_t t) {
+  if (atomicMin(tmin, t) > t)
+    for (uint32_t p = 0; p < C.npeers; ++p) atomicMin_system(C.peer_tmin[p], t);
+}
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
@@ -79,6 +91,12 @@ __device__ __forceinline__ double ld_acquire_gpu_f64(const double* p) {
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// System scope: a peer GPU may lower the word (spec_falsify) over NVLink.
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 // Lock-free pre-check of a (fit, particle) record that only grows in beats()

@@ -192,6 +192,13 @@ class Swarm:
         check(lib().cupso_nccl_init(self._h, buf, nranks, rank))
 
 
+def link_shards(shards: list["Swarm"]) -> None:
+    """Shards of one swarm in this process: a falsified speculative pass on one
+    stops the others early (cupso_shard_link; results never depend on it)."""
+    arr = (C.c_void_p * len(shards))(*[sh._h for sh in shards])
+    check(lib().cupso_shard_link(arr, len(shards)))
+
+
 def init_shards(shards: list["Swarm"]) -> None:
     """(Re)initialise host-exchanged shards: local init_swarm, then every shard
     adopts the swarm-wide initial gbest."""

@@ -60,16 +60,19 @@ class _ThreadAllGather:
         return out
 
 
-@pytest.mark.parametrize("fitness,n,d,T,shards,mode", [("sphere", 20001, 8, 60, 2, "auto"),
-                                                        ("cubic", 65536, 1, 80, 4, "auto"),
-                                                        ("rastrigin", 3001, 32, 40, 3, "auto"),
-                                                        ("rosenbrock", 5001, 5, 50, 2, "auto"),
-                                                        ("sphere", 3001, 4, 30, 2, "wave")])
-def test_shards_step_exchange_equal_single_swarm(cupso, monkeypatch, fitness, n, d, T, shards, mode):
+@pytest.mark.parametrize("fitness,n,d,T,shards,mode,link", [("sphere", 20001, 8, 60, 2, "auto", False),
+                                                             ("sphere", 20001, 8, 60, 3, "auto", True),
+                                                             ("cubic", 65536, 1, 80, 4, "auto", True),
+                                                             ("rastrigin", 3001, 32, 40, 3, "auto", True),
+                                                             ("rosenbrock", 5001, 5, 50, 2, "auto", False),
+                                                             ("rosenbrock", 5001, 5, 50, 4, "auto", True),
+                                                             ("sphere", 3001, 4, 30, 2, "wave", False)])
+def test_shards_step_exchange_equal_single_swarm(cupso, monkeypatch, fitness, n, d, T, shards, mode, link):
     """The sharded speculative protocol on the device (k_spec with a pass record,
     all-gather, k_spec_commit on every shard) with the all-gather done by host
     threads: G shards on one GPU == one swarm, bitwise (trace, gbest index
-    trajectory, every shard's state). mode=wave: the per-iteration protocol."""
+    trajectory, every shard's state), with and without the cross-shard early-stop
+    links. mode=wave: the per-iteration protocol."""
     import threading
     monkeypatch.setenv("CUPSO_SYNC_MODE", mode)
     f = cupso.find_fitness(fitness)
@@ -82,6 +85,8 @@ def test_shards_step_exchange_equal_single_swarm(cupso, monkeypatch, fitness, n,
              for a, c in (cupso.shard_range(n, shards, r) for r in range(shards))]
     try:
         cupso.init_shards(parts)
+        if link:  # falsified passes stop every shard early (cupso_shard_link)
+            cupso.link_shards(parts)
         ag = _ThreadAllGather(shards)
         errs = []
 
