@@ -368,6 +368,13 @@ def main():
                                 "below alg bytes = L2-resident state, above = pbest write-backs",
                 "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
                 "bytes_per_particle_update": bytes_per_pu}
+    # RNG ceiling: the reference's two Philox-4x32-10 calls per particle-axis alone
+    # run at 3.11e11 draw pairs/s on a B200 (profiles/micro_philox_r01.txt); the
+    # FP32 engine draws one call per particle-axis
+    draws_ps = 3.114e11 * (2.0 if f32 else 1.0)
+    roofline["rng_ceiling"] = {"bound": "issue (Philox IMAD.WIDE/LOP3)", "achieved": value,
+                               "peak": draws_ps / d, "unit": "particle-updates/s", "frac": value / (draws_ps / d),
+                               "source": "profiles/micro_philox_r01.txt (draw-only microbenchmark, 1 GPU)"}
     if spec:
         roofline["spec"] = {"passes_per_step": spec_passes, "launches_per_step": spec_launches,
                             "falsified_per_step": (spec1[1] - spec0[1]) / K,
