@@ -372,8 +372,9 @@ def main():
     # run at 3.11e11 draw pairs/s on a B200 (profiles/micro_philox_r01.txt); the
     # FP32 engine draws one call per particle-axis
     draws_ps = 3.114e11 * (2.0 if f32 else 1.0)
+    rng_peak = draws_ps / d * world  # whole job
     roofline["rng_ceiling"] = {"bound": "issue (Philox IMAD.WIDE/LOP3)", "achieved": value,
-                               "peak": draws_ps / d, "unit": "particle-updates/s", "frac": value / (draws_ps / d),
+                               "peak": rng_peak, "unit": "particle-updates/s", "frac": value / rng_peak,
                                "source": "profiles/micro_philox_r01.txt (draw-only microbenchmark, 1 GPU)"}
     if spec:
         roofline["spec"] = {"passes_per_step": spec_passes, "launches_per_step": spec_launches,
