@@ -691,6 +691,7 @@ SpecPick spec_kernel(uint32_t d, uint32_t n, int nsm) {
     case 32: return split_pick<F, 8, 4, 2, false>();
     case 64: return split_pick<F, 8, 8, 2, false>();
   }
+  if (k.fn) return k;
   // any other d up to 256: 8 axis slots per lane, the tail lanes ragged
   if (d <= 8) return split_pick<F, 8, 1, 2, false, true>();
   if (d <= 16) return split_pick<F, 8, 2, 2, false, true>();
@@ -699,6 +700,24 @@ SpecPick spec_kernel(uint32_t d, uint32_t n, int nsm) {
   if (d <= 128) return split_pick<F, 8, 16, 2, false, true>();
   if (d <= 256) return split_pick<F, 8, 32, 2, false, true>();
   return k;
+}
+
+// Grid of the register-resident pass kernels (grid-stride over thread units).
+// Default: every SM gets the same number of resident blocks (the work per SM
+// then differs by at most one unit per thread). CUPSO_GRID_POLICY=balanced
+// instead equalises units per thread, which can leave SMs with fewer blocks
+// (2^20 d = 1: 256 blocks on 148 SMs -> 13 % idle).
+uint64_t pass_grid(uint64_t units, int per_sm, int nsm) {
+  const uint64_t full = static_cast<uint64_t>(per_sm) * nsm;
+  const uint64_t need = (units + kSyncThreads - 1) / kSyncThreads;
+  const char* e = getenv("CUPSO_GRID_POLICY");
+  if (e && !strcmp(e, "balanced")) {
+    const uint64_t resident = full * kSyncThreads;
+    const uint64_t rounds = (units + resident - 1) / resident;
+    const uint64_t threads = (units + rounds - 1) / rounds;
+    return std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads);
+  }
+  return std::max<uint64_t>(1, std::min(full, need));
 }
 
 // NCCL shards: map every other rank's SpecCtl (CUDA IPC over NVLink) so a
@@ -764,12 +783,8 @@ bool spec_fits(cupso_swarm* h) {
     return false;
   }
   h->spec_smem = k.smem;
-  // balanced grid: every thread takes the same number of units (g lanes per unit)
-  const uint64_t units = (h->P.n + np - 1ull) / np * g;
-  const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
-  const uint64_t rounds = (units + resident - 1) / resident;
-  const uint64_t threads = (units + rounds - 1) / rounds;
-  const uint64_t grid = std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads);
+  const uint64_t units = (h->P.n + np - 1ull) / np * g;  // g lanes per unit
+  const uint64_t grid = pass_grid(units, per_sm, num_sms(h->device));
   // second state buffer (the pass writes B while A stays intact for a re-run)
   const size_t cells = h->P.ld * h->P.d;
   void *pos = nullptr, *vel = nullptr, *pb = nullptr, *pbf = nullptr, *ctl = nullptr, *host = nullptr;
@@ -911,10 +926,7 @@ bool async_reg_fits(cupso_swarm* h) {
     return false;
   }
   const uint64_t units = (h->P.n + np - 1ull) / np;
-  const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
-  const uint64_t rounds = (units + resident - 1) / resident;
-  const uint64_t threads = (units + rounds - 1) / rounds;
-  h->areg_grid = static_cast<int>(std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads));
+  h->areg_grid = static_cast<int>(pass_grid(units, per_sm, num_sms(h->device)));
   const char* k = getenv("CUPSO_ASYNC_K");
   h->areg_k = k ? std::max(1, atoi(k)) : 32;
   return true;
@@ -1053,10 +1065,7 @@ cupso_status ensure_f32(cupso_swarm* h) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->f32_kfn, kSyncThreads, 0));
     if (per_sm < 1) return fail(CUPSO_ECUDA, "cuda-sync-f32: kernel cannot be resident");
     const uint64_t units = (h->P.n + np - 1ull) / np;
-    const uint64_t resident = static_cast<uint64_t>(per_sm) * num_sms(h->device) * kSyncThreads;
-    const uint64_t rounds = (units + resident - 1) / resident;
-    const uint64_t threads = (units + rounds - 1) / rounds;
-    h->f32_grid = static_cast<int>(std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads));
+    h->f32_grid = static_cast<int>(pass_grid(units, per_sm, num_sms(h->device)));
   } else {
     h->f32_grid = static_cast<int>(std::min<uint64_t>((h->P.n + kSyncThreads - 1) / kSyncThreads,
                                                      static_cast<uint64_t>(num_sms(h->device)) * 8));

@@ -64,6 +64,9 @@ struct KCtl {
 };
 
 // Lower this shard's tmin and, when that was news, the peers' (rare path).
+// The peer atomics execute at the owning GPU's L2 (NVLink P2P), so the
+// owner's gpu-scope polls see them; polling at sys scope instead measured 2x
+// slower passes (every poll leaves the GPU).
 __device__ __forceinline__ void spec_falsify(const KCtl& C, uint32_t* tmin, uint32_t t) {
   if (atomicMin(tmin, t) > t)
     for (uint32_t p = 0; p < C.npeers; ++p) atomicMin_system(C.peer_tmin[p], t);
@@ -91,12 +94,6 @@ __device__ __forceinline__ double ld_acquire_gpu_f64(const double* p) {
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// System scope: a peer GPU may lower the word (spec_falsify) over NVLink.
-__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 // Lock-free pre-check of a (fit, particle) record that only grows in beats()

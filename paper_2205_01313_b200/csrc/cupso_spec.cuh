@@ -247,11 +247,11 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
   for (int a = 0; a < D; ++a) gp[a] = s_gpos[a];
   double bf = -INFINITY;
   uint32_t bi = kNoParticle, adm = 0;
-  uint32_t tstop = ld_relaxed_sys(&sc->tmin);
+  uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
   const uint32_t units = (P.n + NP - 1) / NP;
   const size_t ld = P.ld;
   for (uint32_t u = blockIdx.x * blockDim.x + tid; u < units; u += gridDim.x * blockDim.x) {
-    tstop = min(tstop, ld_relaxed_sys(&sc->tmin));
+    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
     uint32_t te = min(t0 + K, tstop);  // iterations >= tstop cannot change the outcome
     if (te <= t0) break;               // the pass already failed at t0
     const uint32_t li = NP * u, g0 = P.base + li;
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
         break;
       }
       if (((t - t0) & 15u) == 15u) {
-        tstop = min(tstop, ld_relaxed_sys(&sc->tmin));
+        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
         te = min(te, tstop);
       }
     }
@@ -389,13 +389,13 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
   for (int a = 0; a < DL; ++a) gp[a] = s_gpos[a0 + a];
   double bf = -INFINITY;
   uint32_t bi = kNoParticle, adm = 0;
-  uint32_t tstop = ld_relaxed_sys(&sc->tmin);
+  uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
   const uint32_t per_warp = 32 / G;
   const uint32_t stride = gridDim.x * (blockDim.x / G);
   const size_t ld = P.ld;
   // warp-uniform particle loop: particle = u0 + lane / G
   for (uint32_t u0 = (blockIdx.x * blockDim.x + (tid & ~31u)) / G; u0 < P.n; u0 += stride) {
-    tstop = min(tstop, ld_relaxed_sys(&sc->tmin));
+    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
     uint32_t te = min(t0 + K, tstop);
     if (te <= t0) break;  // warp-uniform: one load serves the warp
     const uint32_t li = u0 + lane / G;
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
         break;
       }
       if (((t - t0) & 15u) == 15u) {
-        tstop = min(tstop, ld_relaxed_sys(&sc->tmin));
+        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
         te = min(te, tstop);
       }
     }

@@ -194,3 +194,20 @@ def test_spec_d1_unit_policy(cupso, oracle, spec_env, n):
     assert np.array_equal(got["trace_particle"], orc.trace_particle)
     if n < 100000:
         compare_state(got["state"], orc, "sphere", f"n={n}")
+
+
+@pytest.mark.parametrize("fit,n,d,T,floor", [("cubic", 1 << 20, 1, 400, 1.0e11), ("sphere", 1 << 22, 8, 24, 1.0e10),
+                                             ("cubic", 1 << 16, 1, 2000, 5.0e10)])
+def test_spec_throughput_floor(cupso, fit, n, d, T, floor):
+    """Regression guard for the kernel choice: the register-resident k_spec runs
+    these shapes at 1.6e11 / 1.7e10 / 9.6e10 p-u/s on a B200; a fall-back to a
+    slower kernel family (e.g. the ragged split kernel for d = 1) halves that."""
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, 1) as sw:
+        best = 1e9
+        for _ in range(2):
+            sw.init()
+            best = min(best, sw.step(cupso.SYNC, T))
+        assert sw.sync_mode() == "spec"
+    assert n * T / best > floor, f"{n * T / best:.3e} p-u/s"
