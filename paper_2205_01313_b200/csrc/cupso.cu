@@ -1569,6 +1569,8 @@ cupso_status cupso_shard_link(cupso_swarm** shards, uint32_t n) {
   if (!shards || n < 1 || n > 16) return fail(CUPSO_EINVAL, "cupso_shard_link: 1..16 shards");
   for (uint32_t i = 0; i < n; ++i) {
     if (!shards[i]) return fail(CUPSO_EINVAL, "null shard handle");
+    if (shards[i]->comm)
+      return fail(CUPSO_EINVAL, "cupso_shard_link: NCCL shards link their peers themselves (CUDA IPC)");
     CK(cudaSetDevice(shards[i]->device));
     if (!spec_fits(shards[i])) return CUPSO_OK;  // no speculative passes on this shape: nothing to link
   }
