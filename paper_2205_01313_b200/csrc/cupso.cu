@@ -859,9 +859,11 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   unsigned char* rec = h->spec_rec_local;
   void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec, &sharded};
   const size_t rb = spec_rec_bytes(h->P.d);
+  const bool trace_passes = getenv("CUPSO_SPEC_TRACE") != nullptr;  // exploration: one line per pass
   for (;;) {
     // passes still needed if no speculation fails from here on
     uint32_t n = 0, t = c.t0, K = c.K, ks = c.kspec;
+    if (trace_passes) n = 1, t = t1;  // one pass at a time, synchronised
     while (t < t1) {
       t += K;
       ++n;
@@ -878,8 +880,12 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
       }
     }
     h->spec_launches += n;
+    const SpecCtl before = c;
     CK(cudaMemcpyAsync(&c, h->spec_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (trace_passes)
+      fprintf(stderr, "spec pass t0=%u K=%u -> %s (next t0=%u K=%u)\n", before.t0, before.K,
+              c.fails > before.fails ? "FALSIFIED" : "committed", c.t0, c.K);
     if (c.t0 >= t1) break;
   }
   h->spec_passes += c.passes;

@@ -39,7 +39,7 @@ struct SpecCtl {
   uint32_t t0;      // first iteration of the next pass
   uint32_t K;       // its length
   uint32_t parity;  // 0: state in S0, 1: state in S1
-  uint32_t kspec;   // speculation length (doubles on success, halves on failure)
+  uint32_t kspec;   // speculation length (doubles after a quiet pass, halves on failure)
   uint32_t tmin;    // earliest admission seen in the running pass (~0u: none)
   uint32_t passes, fails, pad;
 };
@@ -113,8 +113,11 @@ __device__ void spec_decide(const KParams& P, const KCtl& C, SpecCtl* sc, const 
           C.snap->fit = bf;
           C.snap->particle = bi;
         }
+        // grow the speculation only after a pass whose last iteration left the
+        // gbest alone: while it keeps moving every iteration (cfg5's first
+        // iterations) a longer pass would just be falsified at its first one
         uint32_t ks = ks0;
-        if (K >= ks) ks = min(2 * ks, kmax);
+        if (K >= ks && w < 0) ks = min(2 * ks, kmax);
         const uint32_t tn = t0 + K;
         sc->t0 = tn;
         sc->parity = K == 1 ? par : (par ^ 1u);
