@@ -210,30 +210,39 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParam
           acc[k].add(nx, a);
         }
       }
+      float fv[NP];
+      bool any = false;  // fast path: the snapshot is >= every pbest (see k_spec)
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        const float f = acc[k].value();
-        if (!ok[k]) continue;
-        if (f > pbf[k]) {
-          dirty = true;
-          pbf[k] = f;
+        fv[k] = acc[k].value();
+        any |= ok[k] && fv[k] > pbf[k];
+      }
+      if (any) {
 #pragma unroll
-          for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
-        }
-        if (f > snap_fit) {
-          if (t < tl) {
-            bad = true;
-          } else {
-            ++adm;
-            const unsigned long long kk = key32(f, g0 + k);
-            bkey = kk > bkey ? kk : bkey;
+        for (int k = 0; k < NP; ++k) {
+          const float f = fv[k];
+          if (!ok[k]) continue;
+          if (f > pbf[k]) {
+            dirty = true;
+            pbf[k] = f;
+#pragma unroll
+            for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+          }
+          if (f > snap_fit) {
+            if (t < tl) {
+              bad = true;
+            } else {
+              ++adm;
+              const unsigned long long kk = key32(f, g0 + k);
+              bkey = kk > bkey ? kk : bkey;
+            }
           }
         }
-      }
-      if (bad) {
-        atomicMin(&sc->tmin, t);
-        tstop = t;
-        break;
+        if (bad) {
+          atomicMin(&sc->tmin, t);
+          tstop = t;
+          break;
+        }
       }
       if (((t - t0) & 15u) == 15u) {
         tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));

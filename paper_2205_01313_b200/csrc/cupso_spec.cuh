@@ -286,32 +286,45 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
           acc[k].add(x[a][k], a);
         }
       }
+      // Fast path: no particle improved its pbest. The snapshot is the max of
+      // the pbests when the pass starts and an admission before the last
+      // iteration ends it, so f > snapshot implies f > pbest: one compare per
+      // particle decides the common case (nothing to do) in a single branch.
+      double fv[NP];
+      bool any = false;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        const double f = acc[k].value();
-        if (!ok[k]) continue;
-        if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
-          dirty = true;
-          pbf[k] = f;
+        fv[k] = acc[k].value();
+        any |= ok[k] && fv[k] > pbf[k];
+      }
+      if (any) {
 #pragma unroll
-          for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
-        }
-        if (f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
-          if (t < tl) {
-            bad = true;
-          } else {
-            ++adm;
-            if (beats(f, g0 + k, bf, bi)) {
-              bf = f;
-              bi = g0 + k;
+        for (int k = 0; k < NP; ++k) {
+          const double f = fv[k];
+          if (!ok[k]) continue;
+          if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
+            dirty = true;
+            pbf[k] = f;
+#pragma unroll
+            for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+          }
+          if (f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+            if (t < tl) {
+              bad = true;
+            } else {
+              ++adm;
+              if (beats(f, g0 + k, bf, bi)) {
+                bf = f;
+                bi = g0 + k;
+              }
             }
           }
         }
-      }
-      if (bad) {
-        spec_falsify(C, &sc->tmin, t);
-        tstop = t;
-        break;
+        if (bad) {
+          spec_falsify(C, &sc->tmin, t);
+          tstop = t;
+          break;
+        }
       }
       if (((t - t0) & 15u) == 15u) {
         tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
@@ -698,21 +711,32 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KSt
           }
         }
         uint32_t adm = 0;
+        // fast path as in k_spec: the view is >= every pbest of this thread,
+        // so "no pbest improved" covers "nothing admitted" too
+        double fv[NP];
+        bool any = false;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
-          const double f = acc[k].value();
-          if (!ok[k]) continue;
-          if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
-            dirty = true;
-            pbf[k] = f;
+          fv[k] = acc[k].value();
+          any |= ok[k] && fv[k] > pbf[k];
+        }
+        if (any) {
 #pragma unroll
-            for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
-          }
-          if (f > gfit) {  // beats this thread's view of the gbest: it becomes the view
-            ++adm;
-            gfit = f;
+          for (int k = 0; k < NP; ++k) {
+            const double f = fv[k];
+            if (!ok[k]) continue;
+            if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
+              dirty = true;
+              pbf[k] = f;
 #pragma unroll
-            for (int a = 0; a < D; ++a) gp[a] = x[a][k];
+              for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+            }
+            if (f > gfit) {  // beats this thread's view of the gbest: it becomes the view
+              ++adm;
+              gfit = f;
+#pragma unroll
+              for (int a = 0; a < D; ++a) gp[a] = x[a][k];
+            }
           }
         }
         if (adm) {  // rare after warm-up; one atomic per warp
