@@ -301,6 +301,16 @@ void key_schedule(uint64_t seed, KParams& P) {
   }
 }
 
+// c1 / c2 pre-scaled by 2^-53 for vel_step53; exact unless the scaling
+// underflows (|c| < 2^-969), in which case the register-resident kernels
+// (which rely on it) are not used.
+void scale_draws(KParams& P) {
+  P.c1s = std::ldexp(P.c1, -53);
+  P.c2s = std::ldexp(P.c2, -53);
+  auto exact = [](double c) { return c == 0.0 || !std::isfinite(c) || std::fabs(c) >= std::ldexp(1.0, -969); };
+  P.scaled_ok = exact(P.c1) && exact(P.c2);
+}
+
 int num_sms(int device) {
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -768,6 +778,7 @@ void link_ipc_peers(cupso_swarm* h) {
 bool spec_fits(cupso_swarm* h) {
   if (h->spec_checked) return h->spec_grid > 0;
   h->spec_checked = true;
+  if (!h->P.scaled_ok) return false;  // vel_step53 would not be exact
   if (const char* e = getenv("CUPSO_SYNC_MODE"))
     if (strcmp(e, "spec") != 0 && strcmp(e, "auto") != 0) return false;
   SpecPick k;
@@ -920,6 +931,7 @@ const void* async_reg_kernel(uint32_t d, int* np) {
 bool async_reg_fits(cupso_swarm* h) {
   if (h->areg_checked) return h->areg_grid > 0;
   h->areg_checked = true;
+  if (!h->P.scaled_ok) return false;
   const char* mode = getenv("CUPSO_ASYNC_MODE");
   if (mode && strcmp(mode, "reg") != 0 && strcmp(mode, "auto") != 0) return false;
   const void* kfn = nullptr;
@@ -1271,6 +1283,7 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   P.gs = p->group_size;
   P.ld = (static_cast<uint64_t>(count) + 63) / 64 * 64;
   key_schedule(seed, P);
+  scale_draws(P);
   h->step_cfg = default_step_cfg(P);
   h->wave = use_wave(P);
   h->wave_cfg = default_wave_cfg();

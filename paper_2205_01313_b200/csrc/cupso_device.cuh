@@ -28,6 +28,11 @@ struct KParams {
   uint32_t base;                    // global index of local particle 0 (multi-GPU shards)
   uint32_t gs;                      // group_size for the classic engines
   uint32_t k0[10], k1[10];          // Philox key schedule (seed-only, precomputed on host)
+  // c1 * 2^-53 and c2 * 2^-53 (exact power-of-two scalings; scaled_ok when no
+  // underflow): c1 * r1 == c1s * b1 bit for bit where r1 = b1 * 2^-53, so the
+  // register-resident kernels skip the two scaling multiplies per particle-axis
+  double c1s, c2s;
+  uint32_t scaled_ok;
 };
 
 // Axis-major SoA state, row stride ld (flat index = axis*ld + i).
@@ -65,6 +70,15 @@ __device__ __forceinline__ double uniform01(const KParams& P, uint32_t t, uint32
   return __dmul_rn(__ull2double_rn(bits53), 0x1.0p-53);
 }
 
+// The 53-bit integer behind uniform01 as a double (exact: < 2^53): uniform01 ==
+// uniform53 * 2^-53 exactly.
+__device__ __forceinline__ double uniform53(const KParams& P, uint32_t t, uint32_t i, uint32_t axis,
+                                            uint32_t slot) {
+  uint32_t c0 = t, c1 = i, c2 = axis, c3 = slot;
+  philox10(c0, c1, c2, c3, P);
+  return __ull2double_rn((static_cast<uint64_t>(c0) << 21) | (c1 >> 11));
+}
+
 // ---------------------------------------------------------- kinematics
 // std::clamp(v, lo, hi): v < lo ? lo : (hi < v ? hi : v)  -- keeps -0.0 and NaN as the CPU does
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
@@ -77,6 +91,16 @@ __device__ __forceinline__ double vel_step(const KParams& P, double v, double x,
   const double a = __dmul_rn(P.w, v);
   const double b = __dmul_rn(__dmul_rn(P.c1, r1), __dsub_rn(pb, x));
   const double c = __dmul_rn(__dmul_rn(P.c2, r2), __dsub_rn(g, x));
+  return clampd(__dadd_rn(__dadd_rn(a, b), c), P.min_v, P.max_v);
+}
+
+// vel_step with the draws as 53-bit integers (uniform53) and c1s / c2s:
+// (c1s * b1) == (c1 * r1) exactly, so the result is vel_step's bit for bit.
+__device__ __forceinline__ double vel_step53(const KParams& P, double v, double x, double pb, double g,
+                                             double b1, double b2) {
+  const double a = __dmul_rn(P.w, v);
+  const double b = __dmul_rn(__dmul_rn(P.c1s, b1), __dsub_rn(pb, x));
+  const double c = __dmul_rn(__dmul_rn(P.c2s, b2), __dsub_rn(g, x));
   return clampd(__dadd_rn(__dadd_rn(a, b), c), P.min_v, P.max_v);
 }
 

@@ -279,9 +279,9 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
       for (int a = 0; a < D; ++a) {
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
-          const double r1 = uniform01(P, t, g0 + k, a, 0);
-          const double r2 = uniform01(P, t, g0 + k, a, 1);
-          v[a][k] = vel_step(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
+          const double r1 = uniform53(P, t, g0 + k, a, 0);
+          const double r2 = uniform53(P, t, g0 + k, a, 1);
+          v[a][k] = vel_step53(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
           x[a][k] = pos_step(P, x[a][k], v[a][k]);
           acc[k].add(x[a][k], a);
         }
@@ -457,10 +457,10 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
         double* tcol = s_state + (3 * DL) * bd + tid;  // TW * DL doubles, stride bd
 #pragma unroll 2
         for (int a = 0; a < DL; ++a) {
-          const double r1 = uniform01(P, t, gi, a0 + a, 0);
-          const double r2 = uniform01(P, t, gi, a0 + a, 1);
+          const double r1 = uniform53(P, t, gi, a0 + a, 0);
+          const double r2 = uniform53(P, t, gi, a0 + a, 1);
           const double x0 = X(a);
-          const double nv = vel_step(P, V(a), x0, PB(a), s_gpos[a0 + a], r1, r2);
+          const double nv = vel_step53(P, V(a), x0, PB(a), s_gpos[a0 + a], r1, r2);
           const double nx = pos_step(P, x0, nv);
           V(a) = nv;
           X(a) = nx;
@@ -494,10 +494,10 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
 #pragma unroll
         for (int a = 0; a < DL; ++a) {
           if (!valid(a)) continue;  // ragged tail: warp-uniform per lane group
-          const double r1 = uniform01(P, t, gi, a0 + a, 0);
-          const double r2 = uniform01(P, t, gi, a0 + a, 1);
+          const double r1 = uniform53(P, t, gi, a0 + a, 0);
+          const double r2 = uniform53(P, t, gi, a0 + a, 1);
           const double x0 = X(a);
-          const double nv = vel_step(P, V(a), x0, PB(a), gp[a], r1, r2);
+          const double nv = vel_step53(P, V(a), x0, PB(a), gp[a], r1, r2);
           const double nx = pos_step(P, x0, nv);
           V(a) = nv;
           X(a) = nx;
@@ -703,9 +703,9 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KSt
         for (int a = 0; a < D; ++a) {
 #pragma unroll
           for (int k = 0; k < NP; ++k) {
-            const double r1 = uniform01(P, t, g0 + k, a, 0);
-            const double r2 = uniform01(P, t, g0 + k, a, 1);
-            v[a][k] = vel_step(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
+            const double r1 = uniform53(P, t, g0 + k, a, 0);
+            const double r2 = uniform53(P, t, g0 + k, a, 1);
+            v[a][k] = vel_step53(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
             x[a][k] = pos_step(P, x[a][k], v[a][k]);
             acc[k].add(x[a][k], a);
           }

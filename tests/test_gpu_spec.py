@@ -211,3 +211,22 @@ def test_spec_throughput_floor(cupso, fit, n, d, T, floor):
             best = min(best, sw.step(cupso.SYNC, T))
         assert sw.sync_mode() == "spec"
     assert n * T / best > floor, f"{n * T / best:.3e} p-u/s"
+
+
+def test_spec_needs_exact_draw_scaling(cupso):
+    """A cognitive / social factor whose 2^-53 scaling would underflow (|c| < 2^-969)
+    keeps cuda-sync off the register kernels (vel_step53 would not be exact);
+    the other modes still match the reduction engine bit for bit."""
+    f = cupso.find_fitness("sphere")
+    base = cupso.make_params(f, 2000, 4, 30)
+    p = cupso.pso_params(**{**base.__dict__, "cognitive": 1e-300}) if hasattr(base, "__dict__") else None
+    if p is None:
+        pytest.skip("pso_params is not a plain record")
+    out = {}
+    for v in (cupso.SYNC, cupso.REDUCTION):
+        with cupso.Swarm(p, f, 4) as sw:
+            sw.step(v, 30)
+            out[v] = sw.trace()[0]
+            if v == cupso.SYNC:
+                assert sw.sync_mode() != "spec"
+    assert_bitwise(out[cupso.SYNC], out[cupso.REDUCTION], "trace")
