@@ -200,6 +200,14 @@ typedef int (*cupso_exchange_fn)(const void* local, void* all, size_t bytes, voi
  * word). An optimisation only -- results never depend on it. NCCL shards do the
  * same through CUDA IPC at their first speculative step. */
 cupso_status cupso_shard_link(cupso_swarm** shards, uint32_t n);
+/* In-process shards (same GPU or peer-accessible GPUs): exchange the pass
+ * records inside the pass kernel over peer memory -- the last block of each
+ * shard's k_spec pushes its record into every shard's mailbox and waits for
+ * theirs, then decides; no all-gather, no commit launch. Each shard must then be
+ * stepped (cupso_step, CUPSO_SYNC) from its own host thread, all with the same
+ * iteration counts. Also links the early-stop hints (cupso_shard_link). NCCL
+ * ranks opt in with CUPSO_SPEC_EXCHANGE=p2p (CUDA IPC). */
+cupso_status cupso_shard_p2p(cupso_swarm** shards, uint32_t n);
 cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks, cupso_exchange_fn fn,
                                  void* user, double* device_seconds);
 

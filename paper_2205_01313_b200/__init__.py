@@ -13,7 +13,7 @@ from .engine import (FIT_SENTINEL, NO_PARTICLE, device_count, engine_entry, engi
                      swarm_state)
 from .protocol import (bench_config, bench_record, csv_header, read_csv, render_table, run_bench,
                        trace_checksum, trimmed_mean, write_csv_row)
-from .swarm import (Swarm, decode_record, encode_record, init_shards, link_shards, nccl_unique_id, select_winner,
+from .swarm import (Swarm, decode_record, encode_record, init_shards, link_shards, nccl_unique_id, p2p_shards, select_winner,
                     shard_range, step_shards)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

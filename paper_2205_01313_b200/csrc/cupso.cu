@@ -178,6 +178,8 @@ struct cupso_swarm {
   uint32_t xranks = 0;
   std::vector<unsigned char> xlocal, xall;
   std::vector<void*> ipc_opened;      // peer SpecCtl mappings (CUDA IPC)
+  bool p2p = false;                   // pass records exchanged in-kernel over peer memory
+  unsigned char* p2p_buf = nullptr;   // mailbox [2][n] records + flags [n+1]
   unsigned char* xrec_dev = nullptr;  // [xranks] gathered records on the device
   size_t xrec_cap = 0;
   unsigned char* spec_rec_local = nullptr;  // this shard's SpecRec of the running pass
@@ -735,44 +737,109 @@ uint64_t pass_grid(uint64_t units, int per_sm, int nsm) {
 // this once, collectively (one all-gather of the 64-byte IPC handles); any
 // failure leaves npeers = 0 -- the hints are an optimisation, never needed
 // for the result. CUPSO_SPEC_PEERS=0 disables.
-void link_ipc_peers(cupso_swarm* h) {
-  h->C.npeers = 0;
-  const char* e = getenv("CUPSO_SPEC_PEERS");
-  const bool want = !(e && !strcmp(e, "0")) && h->nranks > 1 && h->nranks <= 16;
-  // the all-gather runs on every rank whatever it decides, so collectives stay matched
-  struct Slot {
-    cudaIpcMemHandle_t hnd;
-    int ok;
-    int pad[15];
-  };
-  Slot mine{};
-  mine.ok = want && cudaIpcGetMemHandle(&mine.hnd, h->spec_ctl) == cudaSuccess;
-  cudaGetLastError();
+// Mailbox [2][n] pass records (double-buffered by exchange parity) followed
+// by n + 1 flag words, zeroed.
+size_t p2p_bytes(const cupso_swarm* h, uint32_t n) {
+  return (2ull * n * spec_rec_bytes(h->P.d) + 15) / 16 * 16 + 4ull * (n + 1);
+}
+uint32_t* p2p_flags(const cupso_swarm* h, unsigned char* buf, uint32_t n) {
+  return reinterpret_cast<uint32_t*>(buf + (2ull * n * spec_rec_bytes(h->P.d) + 15) / 16 * 16);
+}
+
+// A tiny all-gather on the shard's stream, used only during setup.
+bool ipc_allgather(cupso_swarm* h, const void* mine, void* all, size_t bytes) {
   void *dsend = nullptr, *drecv = nullptr;
-  std::vector<Slot> all(h->nranks);
-  bool ok = cudaMalloc(&dsend, sizeof(Slot)) == cudaSuccess &&
-            cudaMalloc(&drecv, sizeof(Slot) * h->nranks) == cudaSuccess &&
-            cudaMemcpyAsync(dsend, &mine, sizeof(Slot), cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
-  ok = ok && nccl().allGather(dsend, drecv, sizeof(Slot), /*ncclInt8*/ 0, h->comm, h->stream) == 0;
-  ok = ok && cudaMemcpyAsync(all.data(), drecv, sizeof(Slot) * h->nranks, cudaMemcpyDeviceToHost, h->stream) ==
-                 cudaSuccess;
+  bool ok = cudaMalloc(&dsend, bytes) == cudaSuccess && cudaMalloc(&drecv, bytes * h->nranks) == cudaSuccess &&
+            cudaMemcpyAsync(dsend, mine, bytes, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
+  ok = ok && nccl().allGather(dsend, drecv, bytes, /*ncclInt8*/ 0, h->comm, h->stream) == 0;
+  ok = ok && cudaMemcpyAsync(all, drecv, bytes * h->nranks, cudaMemcpyDeviceToHost, h->stream) == cudaSuccess;
   ok = ok && cudaStreamSynchronize(h->stream) == cudaSuccess;
   if (dsend) cudaFree(dsend);
   if (drecv) cudaFree(drecv);
-  for (int r = 0; ok && r < h->nranks; ++r) ok = all[r].ok != 0;
+  cudaGetLastError();
+  return ok;
+}
+
+// NCCL shards: map every other rank's SpecCtl (CUDA IPC over NVLink) so a
+// falsified pass stops all shards early (KCtl.peer_tmin), and -- with
+// CUPSO_SPEC_EXCHANGE=p2p -- every rank's pass-record mailbox, so the pass
+// records are exchanged inside k_spec instead of by ncclAllGather +
+// k_spec_commit. Every rank calls this once, collectively (two all-gathers:
+// the IPC handles, then whether every rank mapped every peer -- the exchange
+// mode must agree across ranks). Any failure leaves the hints off and the
+// NCCL exchange in place. CUPSO_SPEC_PEERS=0 disables both.
+void link_ipc_peers(cupso_swarm* h) {
+  h->C.npeers = 0;
+  const char* e = getenv("CUPSO_SPEC_PEERS");
+  const char* x = getenv("CUPSO_SPEC_EXCHANGE");
+  const int n = h->nranks;
+  const bool want = !(e && !strcmp(e, "0")) && n > 1 && n <= 16;
+  const bool want_p2p = want && x && !strcmp(x, "p2p");
+  struct Slot {
+    cudaIpcMemHandle_t ctl, box;
+    int ok, box_ok;
+    int pad[14];
+  };
+  Slot mine{};
+  mine.ok = want && cudaIpcGetMemHandle(&mine.ctl, h->spec_ctl) == cudaSuccess;
+  if (want_p2p && !h->p2p_buf) {
+    void* b = nullptr;
+    if (cudaMalloc(&b, p2p_bytes(h, n)) == cudaSuccess && cudaMemset(b, 0, p2p_bytes(h, n)) == cudaSuccess) {
+      h->allocs.push_back(b);
+      h->p2p_buf = static_cast<unsigned char*>(b);
+    }
+  }
+  mine.box_ok = want_p2p && h->p2p_buf && cudaIpcGetMemHandle(&mine.box, h->p2p_buf) == cudaSuccess;
+  cudaGetLastError();
+  // the all-gathers run on every rank whatever it decided, so collectives stay matched
+  std::vector<Slot> all(n);
+  bool ok = ipc_allgather(h, &mine, all.data(), sizeof(Slot));
+  bool box_ok = ok;
+  for (int r = 0; ok && r < n; ++r) {
+    ok = all[r].ok != 0;
+    box_ok = box_ok && all[r].box_ok != 0;
+  }
+  box_ok = box_ok && ok;
   uint32_t np = 0;
-  for (int r = 0; ok && r < h->nranks; ++r) {
-    if (r == h->rank) continue;
+  std::vector<unsigned char*> boxes(n, nullptr);
+  for (int r = 0; ok && r < n; ++r) {
+    if (r == h->rank) {
+      boxes[r] = h->p2p_buf;
+      continue;
+    }
     void* base = nullptr;
-    if (cudaIpcOpenMemHandle(&base, all[r].hnd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      ok = false;
+    if (cudaIpcOpenMemHandle(&base, all[r].ctl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      ok = box_ok = false;
       break;
     }
     h->ipc_opened.push_back(base);
     h->C.peer_tmin[np++] = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(base) + offsetof(SpecCtl, tmin));
+    if (box_ok) {
+      void* bb = nullptr;
+      if (cudaIpcOpenMemHandle(&bb, all[r].box, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        box_ok = false;
+      } else {
+        h->ipc_opened.push_back(bb);
+        boxes[r] = static_cast<unsigned char*>(bb);
+      }
+    }
   }
   cudaGetLastError();
   h->C.npeers = ok ? np : 0;
+  if (!want_p2p) return;
+  // consensus: the fused exchange only if every rank mapped every mailbox
+  int mine_ok = box_ok ? 1 : 0;
+  std::vector<int> oks(n, 0);
+  bool agree = ipc_allgather(h, &mine_ok, oks.data(), sizeof(int));
+  for (int r = 0; agree && r < n; ++r) agree = oks[r] != 0;
+  if (!agree) return;
+  for (int r = 0; r < n; ++r) {
+    h->C.mbox[r] = boxes[r];
+    h->C.flag[r] = p2p_flags(h, boxes[r], static_cast<uint32_t>(n));
+  }
+  h->C.p2p_n = static_cast<uint32_t>(n);
+  h->C.p2p_rank = static_cast<uint32_t>(h->rank);
+  h->p2p = true;
 }
 
 bool spec_fits(cupso_swarm* h) {
@@ -865,7 +932,7 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   const void* kfn = k.fn;
   const uint32_t kmax = h->spec_kmax;
   KState s0 = h->S, s1 = h->S_alt;
-  int sharded = h->comm != nullptr || h->xfn != nullptr;
+  int sharded = h->comm != nullptr || h->xfn != nullptr || h->p2p;
   const uint32_t nrec = h->comm ? static_cast<uint32_t>(h->nranks) : h->xranks;
   unsigned char* rec = h->spec_rec_local;
   void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec, &sharded};
@@ -883,7 +950,7 @@ cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
     }
     for (uint32_t i = 0; i < n; ++i) {
       CK(cudaLaunchKernel(kfn, dim3(h->spec_grid), dim3(kSyncThreads), args, h->spec_smem, h->stream));
-      if (sharded) {  // one exchange per pass: the shards' records, then the same decision everywhere
+      if (sharded && !h->p2p) {  // one exchange per pass: the shards' records, then the same decision everywhere
         unsigned char* all = nullptr;
         TRY(exchange(h, h->spec_rec_local, rb, &all));
         k_spec_commit<<<1, 256, 0, h->stream>>>(h->P, h->C, h->spec_ctl, all, nrec, t1, kmax);
@@ -1197,7 +1264,9 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   if (iters && variant <= CUPSO_QUEUE_LOCK) TRY(classic_graph(h, variant, t0, iters, &ge));
   // probe outside the timed region (allocates the second state buffer once)
   const bool spec = iters && variant == CUPSO_SYNC && spec_fits(h);
-  const bool shard_x = h->comm || h->xfn;  // exchanged with other shards
+  const bool shard_x = h->comm || h->xfn || h->p2p;  // exchanged with other shards
+  if (h->p2p && variant == CUPSO_SYNC && iters && !spec_fits(h))
+    return fail(CUPSO_ELOGIC, "peer-memory shards step with speculative passes only");
   const bool wave = variant == CUPSO_SYNC && h->wave && !shard_x && !spec;
   if (iters && wave) {
     TRY(wave_graph(h, t0, iters, &ge));
@@ -1582,6 +1651,36 @@ cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks
   h->xfn = nullptr;
   h->xuser = nullptr;
   return st;
+}
+
+cupso_status cupso_shard_p2p(cupso_swarm** shards, uint32_t n) {
+  if (!shards || n < 1 || n > 16) return fail(CUPSO_EINVAL, "cupso_shard_p2p: 1..16 shards");
+  for (uint32_t i = 0; i < n; ++i) {
+    cupso_swarm* h = shards[i];
+    if (!h) return fail(CUPSO_EINVAL, "null shard handle");
+    if (h->comm) return fail(CUPSO_EINVAL, "cupso_shard_p2p: NCCL shards use CUPSO_SPEC_EXCHANGE=p2p");
+    CK(cudaSetDevice(h->device));
+    if (!spec_fits(h))
+      return fail(CUPSO_EINVAL, "cupso_shard_p2p: no speculative kernel for this shape (dims %u)", h->P.d);
+    if (!h->p2p_buf) {
+      void* b;
+      TRY(dmalloc(h, &b, p2p_bytes(h, n)));
+      CK(cudaMemset(b, 0, p2p_bytes(h, n)));
+      h->p2p_buf = static_cast<unsigned char*>(b);
+    }
+  }
+  TRY(cupso_shard_link(shards, n));  // early-stop hints too
+  for (uint32_t i = 0; i < n; ++i) {
+    KCtl& C = shards[i]->C;
+    for (uint32_t r = 0; r < n; ++r) {
+      C.mbox[r] = shards[r]->p2p_buf;
+      C.flag[r] = p2p_flags(shards[r], shards[r]->p2p_buf, n);
+    }
+    C.p2p_n = n;
+    C.p2p_rank = i;
+    shards[i]->p2p = true;
+  }
+  return CUPSO_OK;
 }
 
 cupso_status cupso_shard_link(cupso_swarm** shards, uint32_t n) {

@@ -61,6 +61,13 @@ struct KCtl {
   // decision always comes from the exchanged pass records.
   uint32_t npeers;
   uint32_t* peer_tmin[15];
+  // In-kernel exchange of the pass records over peer memory (replaces the
+  // all-gather + k_spec_commit when p2p_n > 0): rank r's record goes to slot r
+  // of every rank's mailbox, then a release store of the exchange number to
+  // that rank's flag[r]; each rank waits for all flags and decides locally.
+  uint32_t p2p_n, p2p_rank;
+  unsigned char* mbox[16];  // every rank's mailbox ([p2p_n] records)
+  uint32_t* flag[16];       // every rank's flags ([p2p_n] exchange numbers + [1] own counter)
 };
 
 // Lower this shard's tmin and, when that was news, the peers' (rare path).

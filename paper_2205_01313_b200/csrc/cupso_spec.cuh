@@ -149,6 +149,54 @@ __global__ void k_spec_commit(KParams P, KCtl C, SpecCtl* sc, const unsigned cha
   spec_decide(P, C, sc, recs, nrec, t_end, kmax);
 }
 
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The pass-record all-gather over peer memory, run by the last block of every
+// shard's k_spec (one block per rank): push this rank's record into slot
+// p2p_rank of every rank's mailbox, publish exchange number e to each rank's
+// flag[p2p_rank] (release, system scope: peers read it over NVLink), then wait
+// until every rank's flag in the local array reached e. All ranks perform the
+// same sequence of exchanges, so e (a local counter) agrees across ranks.
+// Mailboxes are double-buffered by exchange parity: a rank can write its next
+// record before a slower rank has read this one, but not the one after (that
+// needs the slower rank's next flag).
+__device__ const unsigned char* spec_exchange_p2p(const KParams& P, const KCtl& C, const unsigned char* rec) {
+  __shared__ uint32_t s_e;
+  const uint32_t tid = threadIdx.x, n = C.p2p_n, me = C.p2p_rank;
+  const size_t rb = spec_rec_bytes(P.d);
+  uint32_t* own = C.flag[me];
+  if (tid == 0) {
+    s_e = own[n] + 1u;  // this rank's exchange counter
+    own[n] = s_e;
+  }
+  __syncthreads();
+  const uint32_t e = s_e;
+  const size_t half = (e & 1u) * n * rb;
+  for (uint32_t r = 0; r < n; ++r)  // 8-byte words of the record to every rank (rb % 8 == 0)
+    for (uint32_t w = tid; w < rb / 8; w += blockDim.x)
+      reinterpret_cast<unsigned long long*>(C.mbox[r] + half + me * rb)[w] =
+          reinterpret_cast<const unsigned long long*>(rec)[w];
+  __threadfence_system();
+  __syncthreads();
+  if (tid < n) st_release_sys(C.flag[tid] + me, e);
+  if (tid == 0) {
+    const uint64_t ts = globaltimer_ns();
+    for (uint32_t q = 0; q < n; ++q)
+      while (ld_acquire_sys(own + q) < e)
+        if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+    __threadfence_system();
+  }
+  __syncthreads();
+  return C.mbox[me] + half;
+}
+
 // End of a pass (every block): block winner of the last iteration to the grid
 // queue; the last block to finish reduces the queue to this shard's SpecRec
 // (rec_out) and -- unless the pass is sharded (the host all-gathers the
@@ -210,7 +258,12 @@ __device__ __forceinline__ void spec_finish(const KParams& P, const KState& So, 
     __threadfence();
   }
   __syncthreads();
-  if (!sharded) spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
+  if (sharded && C.p2p_n) {  // the exchange itself, fused into the pass (peer memory)
+    const unsigned char* all = spec_exchange_p2p(P, C, rec_out);
+    spec_decide(P, C, sc, all, C.p2p_n, t_end, kmax);
+  } else if (!sharded) {
+    spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
+  }
 }
 
 // D: dims (compile time; the particle's whole state lives in registers).

@@ -199,6 +199,13 @@ def link_shards(shards: list["Swarm"]) -> None:
     check(lib().cupso_shard_link(arr, len(shards)))
 
 
+def p2p_shards(shards: list["Swarm"]) -> None:
+    """Shards of one swarm in this process exchange their pass records inside the
+    pass kernel over peer memory (cupso_shard_p2p). Step each from its own thread."""
+    arr = (C.c_void_p * len(shards))(*[sh._h for sh in shards])
+    check(lib().cupso_shard_p2p(arr, len(shards)))
+
+
 def init_shards(shards: list["Swarm"]) -> None:
     """(Re)initialise host-exchanged shards: local init_swarm, then every shard
     adopts the swarm-wide initial gbest."""

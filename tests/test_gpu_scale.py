@@ -117,6 +117,51 @@ def test_shards_step_exchange_equal_single_swarm(cupso, monkeypatch, fitness, n,
             sh.close()
 
 
+@pytest.mark.parametrize("fitness,n,d,T,shards", [("sphere", 20001, 8, 60, 2), ("sphere", 30001, 8, 60, 4),
+                                                   ("rosenbrock", 5001, 5, 50, 3), ("cubic", 65536, 1, 80, 2),
+                                                   ("rastrigin", 3001, 32, 40, 3)])
+def test_shards_p2p_exchange_equal_single_swarm(cupso, fitness, n, d, T, shards):
+    """The pass-record exchange fused into the pass kernel (peer-memory mailboxes,
+    cupso_shard_p2p): G shards on one GPU, each stepped from its own thread with no
+    host exchange at all == one swarm, bitwise (trace, trajectory, state)."""
+    import threading
+    f = cupso.find_fitness(fitness)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, 17) as whole:
+        whole.step(cupso.SYNC, T)
+        wtr, wtp, _ = whole.trace()
+        wst = whole.state()
+    parts = [cupso.Swarm(p, f, 17, first=a, count=c, init=False)
+             for a, c in (cupso.shard_range(n, shards, r) for r in range(shards))]
+    try:
+        cupso.init_shards(parts)
+        cupso.p2p_shards(parts)
+        errs = []
+
+        def run(r):
+            try:
+                parts[r].step(cupso.SYNC, T // 3)
+                parts[r].step(cupso.SYNC, T - T // 3)
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(shards)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        assert not errs, errs
+        for sh in parts:
+            tr, tp, _ = sh.trace()
+            assert same(tr, wtr) and np.array_equal(tp, wtp)
+        pos = np.concatenate([sh.state().positions.reshape(d, -1) for sh in parts], axis=1)
+        assert same(pos.reshape(-1), wst.positions)
+        assert parts[0].spec_stats()[0] < T
+    finally:
+        for sh in parts:
+            sh.close()
+
+
 @pytest.mark.parametrize("mode,d,want", [("auto", 4, "nccl-sharded-spec"), ("auto", 32, "nccl-sharded-spec"),
                                          ("auto", 3, "nccl-sharded-spec"), ("wave", 4, "nccl-sharded"),
                                          ("persistent", 3, "nccl-sharded")])
