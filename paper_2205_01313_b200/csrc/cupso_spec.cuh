@@ -453,9 +453,8 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
   const double snap_fit = C.snap->fit;
   const uint32_t tl = t0 + K - 1;
   const uint32_t a0 = sub * DL;  // first axis of this lane
-  double gp[DL];
-#pragma unroll
-  for (int a = 0; a < DL; ++a) gp[a] = s_gpos[a0 + a];
+  // the gbest position is read from SMEM at each use (broadcast LDS): holding
+  // its 8 doubles in registers cost spills (cfg4: 2.7 % slower)
   double bf = -INFINITY;
   uint32_t bi = kNoParticle, adm = 0;
   uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
@@ -550,7 +549,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
           const double r1 = uniform53(P, t, gi, a0 + a, 0);
           const double r2 = uniform53(P, t, gi, a0 + a, 1);
           const double x0 = X(a);
-          const double nv = vel_step53(P, V(a), x0, PB(a), gp[a], r1, r2);
+          const double nv = vel_step53(P, V(a), x0, PB(a), s_gpos[a0 + a], r1, r2);
           const double nx = pos_step(P, x0, nv);
           V(a) = nv;
           X(a) = nx;
