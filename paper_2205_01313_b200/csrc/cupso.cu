@@ -4,8 +4,12 @@
 // a multiple of 64 particles so every row is 512-byte aligned and the
 // two-particle double2 path never straddles a row), a small control block
 // (gbest snapshot/live records, trace arrays, counters) and a stream. A
-// "step" launches one of the six aggregation variants for a range of
-// iterations and times exactly that range with CUDA events.
+// "step" launches one of the seven engines for a range of iterations and
+// times exactly that range with CUDA events. cuda-sync normally runs the
+// speculative register-resident passes of cupso_spec.cuh (second state
+// buffer, device-side pass schedule), cuda-async the register-resident
+// k_async_reg, cuda-sync-f32 the FP32 passes of cupso_f32.cuh; the classic
+// kernels of cupso_kernels.cuh cover the paper's engines and other shapes.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 

@@ -14,6 +14,8 @@
 //   k_async<F>  free-running blocks; the global best is a seqlock record
 //               whose writers take it with a CAS on the version word.
 //   k_propose<F> + k_commit: one iteration of a shard (multi-GPU exchange).
+// The speculative register-resident passes that cuda-sync / cuda-async use for
+// the BASELINE shapes live in cupso_spec.cuh, the FP32 engine in cupso_f32.cuh.
 #pragma once
 
 #include <cfloat>
