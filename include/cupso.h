@@ -55,14 +55,16 @@ typedef struct cupso_params {
 
 /* Aggregation variants ("engines"). The first four restate the reference's
  * parallel engines (engines.hpp:26-37) as classic per-iteration CUDA launches;
- * SYNC and ASYNC are the B200-native persistent kernels. */
+ * SYNC, ASYNC and SYNC_F32 are the B200-native engines (register-resident
+ * speculative passes / free-running register kernels; see cupso_sync_mode). */
 typedef enum cupso_variant {
   CUPSO_REDUCTION = 0,  /* "cuda-reduction": step+block tree, fold kernel  (engine_reduction.hpp:26-93) */
   CUPSO_UNROLLED = 1,   /* "cuda-unrolled" : same, straight-line tree      (engine_reduction.hpp:48-76) */
   CUPSO_QUEUE = 2,      /* "cuda-queue"    : filtered smem queue + fold     (engine_queue.hpp:39-78) */
   CUPSO_QUEUE_LOCK = 3, /* "cuda-queue-lock": fused, lock-guarded commit   (engine_queue.hpp:86-104) */
-  CUPSO_SYNC = 4,       /* "cuda-sync"     : persistent fused kernel, grid queue + grid barrier */
-  CUPSO_ASYNC = 5,      /* "cuda-async"    : persistent free-running blocks, CAS/seqlock gbest */
+  CUPSO_SYNC = 4,       /* "cuda-sync"     : speculative passes of K iterations in registers, exact
+                           re-run when falsified; grid queue per pass (bitwise == run_serial) */
+  CUPSO_ASYNC = 5,      /* "cuda-async"    : free-running register kernel, CAS/seqlock gbest */
   CUPSO_SYNC_F32 = 6    /* "cuda-sync-f32" : FP32 state, packed 64-bit (fitness, index) atomicMax
                            aggregation; statistical (not bitwise) vs the FP64 reference */
 } cupso_variant;
