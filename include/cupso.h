@@ -210,6 +210,14 @@ cupso_status cupso_shard_link(cupso_swarm** shards, uint32_t n);
  * iteration counts. Also links the early-stop hints (cupso_shard_link). NCCL
  * ranks opt in with CUPSO_SPEC_EXCHANGE=p2p (CUDA IPC). */
 cupso_status cupso_shard_p2p(cupso_swarm** shards, uint32_t n);
+/* The same across processes through any host channel (what NCCL shards do
+ * internally): every rank exports a 192-byte record of CUDA IPC handles
+ * (cupso_ipc_handles), the caller all-gathers them in rank order, and every rank
+ * opens its peers' (cupso_ipc_link): early-stop hints always, and with p2p the
+ * pass-record exchange fused into the pass kernel -- then each rank steps with
+ * plain cupso_step (p2p) or cupso_step_exchange (host all-gather). */
+cupso_status cupso_ipc_handles(cupso_swarm* h, uint32_t nranks, int p2p, void* out192);
+cupso_status cupso_ipc_link(cupso_swarm* h, const void* all_handles, uint32_t nranks, uint32_t rank, int p2p);
 cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks, cupso_exchange_fn fn,
                                  void* user, double* device_seconds);
 

@@ -94,6 +94,8 @@ SIGNATURES = {
     "cupso_step_exchange": (C.c_int, [_vp, C.c_uint32, C.c_uint32, EXCHANGE_FN, _vp, _dp]),
     "cupso_shard_link": (C.c_int, [_vp, C.c_uint32]),
     "cupso_shard_p2p": (C.c_int, [_vp, C.c_uint32]),
+    "cupso_ipc_handles": (C.c_int, [_vp, C.c_uint32, C.c_int, _vp]),
+    "cupso_ipc_link": (C.c_int, [_vp, _vp, C.c_uint32, C.c_uint32, C.c_int]),
     "cupso_async_mode": (C.c_int, [_vp]),
     "cupso_record_bytes": (C.c_size_t, [C.c_uint32]),
     "cupso_shard_snapshot": (C.c_int, [_vp, _vp]),

@@ -736,11 +736,6 @@ uint64_t pass_grid(uint64_t units, int per_sm, int nsm) {
   return std::max<uint64_t>(1, std::min(full, need));
 }
 
-// NCCL shards: map every other rank's SpecCtl (CUDA IPC over NVLink) so a
-// falsified pass stops all shards early (KCtl.peer_tmin). Every rank calls
-// this once, collectively (one all-gather of the 64-byte IPC handles); any
-// failure leaves npeers = 0 -- the hints are an optimisation, never needed
-// for the result. CUPSO_SPEC_PEERS=0 disables.
 // Mailbox [2][n] pass records (double-buffered by exchange parity) followed
 // by n + 1 flag words, zeroed.
 size_t p2p_bytes(const cupso_swarm* h, uint32_t n) {
@@ -764,56 +759,51 @@ bool ipc_allgather(cupso_swarm* h, const void* mine, void* all, size_t bytes) {
   return ok;
 }
 
-// NCCL shards: map every other rank's SpecCtl (CUDA IPC over NVLink) so a
-// falsified pass stops all shards early (KCtl.peer_tmin), and -- with
-// CUPSO_SPEC_EXCHANGE=p2p -- every rank's pass-record mailbox, so the pass
-// records are exchanged inside k_spec instead of by ncclAllGather +
-// k_spec_commit. Every rank calls this once, collectively (two all-gathers:
-// the IPC handles, then whether every rank mapped every peer -- the exchange
-// mode must agree across ranks). Any failure leaves the hints off and the
-// NCCL exchange in place. CUPSO_SPEC_PEERS=0 disables both.
-void link_ipc_peers(cupso_swarm* h) {
-  h->C.npeers = 0;
-  const char* e = getenv("CUPSO_SPEC_PEERS");
-  const char* x = getenv("CUPSO_SPEC_EXCHANGE");
-  const int n = h->nranks;
-  const bool want = !(e && !strcmp(e, "0")) && n > 1 && n <= 16;
-  const bool want_p2p = want && x && !strcmp(x, "p2p");
-  struct Slot {
-    cudaIpcMemHandle_t ctl, box;
-    int ok, box_ok;
-    int pad[14];
-  };
-  Slot mine{};
-  mine.ok = want && cudaIpcGetMemHandle(&mine.ctl, h->spec_ctl) == cudaSuccess;
-  if (want_p2p && !h->p2p_buf) {
+
+// CUDA IPC between shard processes (NCCL ranks, or any host channel through
+// cupso_ipc_handles / cupso_ipc_link): each rank exports its SpecCtl and its
+// pass-record mailbox; opening the peers' gives the early-stop hints
+// (KCtl.peer_tmin) and, with p2p, the pass-record exchange fused into k_spec.
+struct IpcSlot {
+  cudaIpcMemHandle_t ctl, box;
+  int ok, box_ok;
+  int pad[14];
+};
+static_assert(sizeof(IpcSlot) == 192, "IpcSlot is part of the cupso_ipc_handles contract");
+
+void ipc_export(cupso_swarm* h, uint32_t n, bool want_box, IpcSlot* mine) {
+  *mine = IpcSlot{};
+  mine->ok = h->spec_ctl && cudaIpcGetMemHandle(&mine->ctl, h->spec_ctl) == cudaSuccess;
+  if (want_box && !h->p2p_buf) {
     void* b = nullptr;
     if (cudaMalloc(&b, p2p_bytes(h, n)) == cudaSuccess && cudaMemset(b, 0, p2p_bytes(h, n)) == cudaSuccess) {
       h->allocs.push_back(b);
       h->p2p_buf = static_cast<unsigned char*>(b);
     }
   }
-  mine.box_ok = want_p2p && h->p2p_buf && cudaIpcGetMemHandle(&mine.box, h->p2p_buf) == cudaSuccess;
+  mine->box_ok = want_box && h->p2p_buf && cudaIpcGetMemHandle(&mine->box, h->p2p_buf) == cudaSuccess;
   cudaGetLastError();
-  // the all-gathers run on every rank whatever it decided, so collectives stay matched
-  std::vector<Slot> all(n);
-  bool ok = ipc_allgather(h, &mine, all.data(), sizeof(Slot));
-  bool box_ok = ok;
-  for (int r = 0; ok && r < n; ++r) {
-    ok = all[r].ok != 0;
-    box_ok = box_ok && all[r].box_ok != 0;
+}
+
+// Open every peer's exports; returns whether all mailboxes were mapped (the
+// hints are set either way, or cleared on failure). The fused exchange is
+// switched on only by the caller, after every rank agreed.
+bool ipc_open(cupso_swarm* h, const IpcSlot* all, uint32_t n, uint32_t rank, std::vector<unsigned char*>& boxes) {
+  bool ok = true, box_ok = true;
+  for (uint32_t r = 0; r < n; ++r) {
+    ok = ok && all[r].ok;
+    box_ok = box_ok && all[r].box_ok;
   }
-  box_ok = box_ok && ok;
   uint32_t np = 0;
-  std::vector<unsigned char*> boxes(n, nullptr);
-  for (int r = 0; ok && r < n; ++r) {
-    if (r == h->rank) {
+  boxes.assign(n, nullptr);
+  for (uint32_t r = 0; ok && r < n; ++r) {
+    if (r == rank) {
       boxes[r] = h->p2p_buf;
       continue;
     }
     void* base = nullptr;
     if (cudaIpcOpenMemHandle(&base, all[r].ctl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      ok = box_ok = false;
+      ok = false;
       break;
     }
     h->ipc_opened.push_back(base);
@@ -830,20 +820,44 @@ void link_ipc_peers(cupso_swarm* h) {
   }
   cudaGetLastError();
   h->C.npeers = ok ? np : 0;
+  return ok && box_ok;
+}
+
+void p2p_enable(cupso_swarm* h, const std::vector<unsigned char*>& boxes, uint32_t n, uint32_t rank) {
+  for (uint32_t r = 0; r < n; ++r) {
+    h->C.mbox[r] = boxes[r];
+    h->C.flag[r] = p2p_flags(h, boxes[r], n);
+  }
+  h->C.p2p_n = n;
+  h->C.p2p_rank = rank;
+  h->p2p = true;
+}
+
+// NCCL shards: the same, collectively at the first speculative step (two
+// all-gathers: the IPC exports, then whether every rank mapped every peer --
+// the exchange mode must agree across ranks). Any failure leaves the hints off
+// and the NCCL exchange in place. CUPSO_SPEC_PEERS=0 disables both,
+// CUPSO_SPEC_EXCHANGE=p2p opts into the fused exchange.
+void link_ipc_peers(cupso_swarm* h) {
+  h->C.npeers = 0;
+  const char* e = getenv("CUPSO_SPEC_PEERS");
+  const char* x = getenv("CUPSO_SPEC_EXCHANGE");
+  const uint32_t n = static_cast<uint32_t>(h->nranks);
+  const bool want = !(e && !strcmp(e, "0")) && n > 1 && n <= 16;
+  const bool want_p2p = want && x && !strcmp(x, "p2p");
+  IpcSlot mine{};
+  if (want) ipc_export(h, n, want_p2p, &mine);
+  // the all-gathers run on every rank whatever it decided, so collectives stay matched
+  std::vector<IpcSlot> all(n);
+  if (!ipc_allgather(h, &mine, all.data(), sizeof(IpcSlot))) return;
+  std::vector<unsigned char*> boxes;
+  const bool box_ok = want && ipc_open(h, all.data(), n, static_cast<uint32_t>(h->rank), boxes);
   if (!want_p2p) return;
-  // consensus: the fused exchange only if every rank mapped every mailbox
   int mine_ok = box_ok ? 1 : 0;
   std::vector<int> oks(n, 0);
   bool agree = ipc_allgather(h, &mine_ok, oks.data(), sizeof(int));
-  for (int r = 0; agree && r < n; ++r) agree = oks[r] != 0;
-  if (!agree) return;
-  for (int r = 0; r < n; ++r) {
-    h->C.mbox[r] = boxes[r];
-    h->C.flag[r] = p2p_flags(h, boxes[r], static_cast<uint32_t>(n));
-  }
-  h->C.p2p_n = static_cast<uint32_t>(n);
-  h->C.p2p_rank = static_cast<uint32_t>(h->rank);
-  h->p2p = true;
+  for (uint32_t r = 0; agree && r < n; ++r) agree = oks[r] != 0;
+  if (agree) p2p_enable(h, boxes, n, static_cast<uint32_t>(h->rank));
 }
 
 bool spec_fits(cupso_swarm* h) {
@@ -1655,6 +1669,32 @@ cupso_status cupso_step_exchange(cupso_swarm* h, uint32_t iters, uint32_t nranks
   h->xfn = nullptr;
   h->xuser = nullptr;
   return st;
+}
+
+cupso_status cupso_ipc_handles(cupso_swarm* h, uint32_t nranks, int p2p, void* out) {
+  if (!h || !out) return fail(CUPSO_EINVAL, "null argument");
+  if (nranks < 1 || nranks > 16) return fail(CUPSO_EINVAL, "cupso_ipc_handles: 1..16 ranks");
+  CK(cudaSetDevice(h->device));
+  if (!spec_fits(h)) return fail(CUPSO_EINVAL, "cupso_ipc_handles: no speculative kernel for this shape");
+  IpcSlot s;
+  ipc_export(h, nranks, p2p != 0, &s);
+  std::memcpy(out, &s, sizeof s);
+  return CUPSO_OK;
+}
+
+cupso_status cupso_ipc_link(cupso_swarm* h, const void* all, uint32_t nranks, uint32_t rank, int p2p) {
+  if (!h || !all) return fail(CUPSO_EINVAL, "null argument");
+  if (nranks < 1 || nranks > 16 || rank >= nranks) return fail(CUPSO_EINVAL, "cupso_ipc_link: bad rank");
+  CK(cudaSetDevice(h->device));
+  std::vector<IpcSlot> slots(nranks);
+  std::memcpy(slots.data(), all, sizeof(IpcSlot) * nranks);
+  std::vector<unsigned char*> boxes;
+  const bool box_ok = ipc_open(h, slots.data(), nranks, rank, boxes);
+  if (p2p) {
+    if (!box_ok) return fail(CUPSO_ERUNTIME, "cupso_ipc_link: a peer mailbox could not be mapped");
+    p2p_enable(h, boxes, nranks, rank);
+  }
+  return CUPSO_OK;
 }
 
 cupso_status cupso_shard_p2p(cupso_swarm** shards, uint32_t n) {

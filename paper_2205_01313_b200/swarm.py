@@ -187,6 +187,20 @@ class Swarm:
         check(st)
         return s.value
 
+    IPC_RECORD = 192  # bytes per rank of cupso_ipc_handles
+
+    def ipc_handles(self, nranks: int, p2p: bool) -> bytes:
+        """This shard's CUDA IPC exports for shards in other processes (cupso_ipc_handles)."""
+        buf = C.create_string_buffer(self.IPC_RECORD)
+        check(lib().cupso_ipc_handles(self._h, nranks, int(p2p), buf))
+        return buf.raw
+
+    def ipc_link(self, all_handles: list[bytes], rank: int, p2p: bool) -> None:
+        """Open the other ranks' exports (rank order): early-stop hints, and with p2p the
+        pass-record exchange fused into the pass kernel (then step with plain step())."""
+        blob = b"".join(all_handles)
+        check(lib().cupso_ipc_link(self._h, blob, len(all_handles), rank, int(p2p)))
+
     def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib().cupso_nccl_init(self._h, buf, nranks, rank))

@@ -454,3 +454,87 @@ def test_cfg3_async_full_size(cupso):
         gb = sw.gbest()
         assert (np.diff(tr) >= 0).all() and tr[-1] == gb.fit == 900000.0
         assert f.eval(gb.pos) == gb.fit
+
+
+# ------------------------------------------------- shards in separate processes
+def _ipc_worker(rank, world, inboxes, out, fitness, n, d, T, p2p):
+    """One shard per process on the same GPU: initial gbest and IPC exports
+    exchanged through multiprocessing queues, then either the fused in-kernel
+    exchange over IPC-mapped mailboxes (p2p) or host all-gathers per pass
+    (cupso_step_exchange) with IPC early-stop hints."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import paper_2205_01313_b200 as cp
+        pending = {}
+        seq = [0]
+
+        def allgather(data):
+            seq[0] += 1
+            for r in range(world):
+                if r != rank:
+                    inboxes[r].put((seq[0], rank, data))
+            got = {rank: data}
+            while len(got) < world:
+                key = next((k for k in pending if k[0] == seq[0]), None)
+                if key is not None:
+                    got[key[1]] = pending.pop(key)
+                    continue
+                s_, src, payload = inboxes[rank].get(timeout=120)
+                if s_ == seq[0]:
+                    got[src] = payload
+                else:
+                    pending[(s_, src)] = payload
+            return [got[r] for r in range(world)]
+
+        f = cp.find_fitness(fitness)
+        p = cp.make_params(f, n, d, T)
+        first, count = cp.shard_range(n, world, rank)
+        sw = cp.Swarm(p, f, 29, device=0, first=first, count=count)
+        sw.adopt(allgather(sw.snapshot_record()))
+        handles = allgather(sw.ipc_handles(world, p2p))
+        sw.ipc_link(handles, rank, p2p)
+        for chunk in (T // 2, T - T // 2):
+            if p2p:
+                sw.step(cp.SYNC, chunk)
+            else:
+                sw.step_exchange(chunk, world, allgather)
+        tr, tp, _ = sw.trace()
+        out.put((rank, tr.tobytes(), tp.tobytes(), sw.state().positions.tobytes(), sw.spec_stats()))
+        sw.close()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        out.put((rank, "error", repr(e), None, None))
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("fitness,n,d,T", [("sphere", 20001, 8, 60), ("rosenbrock", 6001, 4, 50)])
+def test_two_process_ipc_shards_equal_single_swarm(cupso, p2p, fitness, n, d, T):
+    """Two shard processes on one GPU linked through CUDA IPC -- the cross-process
+    path NCCL ranks take (hints; with p2p the exchange fused into k_spec) -- are
+    bitwise equal to the single swarm."""
+    import multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    inboxes = [ctx.Queue() for _ in range(world)]
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, inboxes, out, fitness, n, d, T, p2p))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(out.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in res:
+        assert r[1] != "error", r[2]
+    f = cupso.find_fitness(fitness)
+    with cupso.Swarm(cupso.make_params(f, n, d, T), f, 29) as whole:
+        whole.step(cupso.SYNC, T)
+        wtr, wtp, _ = whole.trace()
+        wpos = whole.state().positions.reshape(d, n)
+    for rank, tr, tp, pos, stats in res:
+        assert np.frombuffer(tr, np.float64).tobytes() == wtr.tobytes(), f"rank {rank} trace"
+        assert np.array_equal(np.frombuffer(tp, np.uint32), wtp), f"rank {rank} trajectory"
+        first, count = cupso.shard_range(n, world, rank)
+        assert np.frombuffer(pos, np.float64).tobytes() == np.ascontiguousarray(wpos[:, first:first + count]).tobytes()
+        assert stats[0] < T
