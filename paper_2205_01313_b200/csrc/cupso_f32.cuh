@@ -5,8 +5,9 @@
 // statistically rather than bitwise:
 //   * state as FP32 SoA rows, 4 adjacent particles per thread moved with one
 //     float4 (LDG.128 / STG.128) per row;
-//   * one Philox-4x32-10 call per (t, particle, axis) -- words 0 and 1 give
-//     r1 and r2 as 24-bit uniforms (the FP64 engines draw two calls, slots 0/1);
+//   * one Philox-4x32-10 call per (iteration pair, particle, axis): words 0/1
+//     give (r1, r2) on the even iteration, words 2/3 on the odd one (the FP64
+//     engines draw two calls per iteration, slots 0/1, using two words each);
 //   * kinematics with FMA and FMNMX clamps, fitness in FP32;
 //   * the gbest aggregation is the paper's atomic scheme on a packed 64-bit
 //     key: (order-preserving FP32 fitness << 32) | ~particle, so one u64
@@ -122,13 +123,25 @@ __device__ __forceinline__ void stv32(float* p, const float (&o)[NP]) {
   }
 }
 
-// One Philox call -> (r1, r2), 24-bit uniforms in [0, 1).
+// The FP32 stream: one Philox call per particle-axis and PAIR of iterations,
+// counter {t/2, particle, axis, 0}; even iterations take words 0/1 as (r1, r2),
+// odd ones words 2/3 -- all four words used, a quarter of the FP64 engines'
+// draw cost. 24-bit uniforms in [0, 1).
+__device__ __forceinline__ float u24(uint32_t w) { return __uint2float_rz(w >> 8) * 0x1.0p-24f; }
+__device__ __forceinline__ void philox_pair(const KParams& P, uint32_t t, uint32_t i, uint32_t axis, uint32_t& w0,
+                                            uint32_t& w1, uint32_t& w2, uint32_t& w3) {
+  w0 = t >> 1;
+  w1 = i;
+  w2 = axis;
+  w3 = 0;
+  philox10(w0, w1, w2, w3, P);
+}
 __device__ __forceinline__ void uniform2_f32(const KParams& P, uint32_t t, uint32_t i, uint32_t axis, float& r1,
                                              float& r2) {
-  uint32_t c0 = t, c1 = i, c2 = axis, c3 = 0;
-  philox10(c0, c1, c2, c3, P);
-  r1 = __uint2float_rz(c0 >> 8) * 0x1.0p-24f;
-  r2 = __uint2float_rz(c1 >> 8) * 0x1.0p-24f;
+  uint32_t w0, w1, w2, w3;
+  philox_pair(P, t, i, axis, w0, w1, w2, w3);
+  r1 = u24((t & 1u) ? w2 : w0);
+  r2 = u24((t & 1u) ? w3 : w1);
 }
 
 // The key slot of the pass lives right after SpecCtl in the control buffer.
@@ -193,14 +206,25 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParam
     for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
     uint32_t t = t0;
     bool bad = false, dirty = false;
+    uint32_t odd_w[D][NP][2];  // words 2/3 of the pair's call, for its odd iteration
     for (; t < te; ++t) {
       Fit32<F> acc[NP];
+      // warp-uniform: a fresh call on even iterations (and on a unit's first)
+      const bool fresh = !(t & 1u) || t == t0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
           float r1, r2;
-          uniform2_f32(P, t, g0 + k, a, r1, r2);
+          if (fresh) {
+            uint32_t w0, w1;
+            philox_pair(P, t, g0 + k, a, w0, w1, odd_w[a][k][0], odd_w[a][k][1]);
+            r1 = u24((t & 1u) ? odd_w[a][k][0] : w0);
+            r2 = u24((t & 1u) ? odd_w[a][k][1] : w1);
+          } else {
+            r1 = u24(odd_w[a][k][0]);
+            r2 = u24(odd_w[a][k][1]);
+          }
           const float xv = x[a][k];
           float nv = __fmaf_rn(Q.c2 * r2, gp[a] - xv, __fmaf_rn(Q.c1 * r1, pb[a][k] - xv, Q.w * v[a][k]));
           nv = fminf(fmaxf(nv, Q.min_v), Q.max_v);
