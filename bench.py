@@ -370,8 +370,8 @@ def main():
                 "bytes_per_particle_update": bytes_per_pu}
     # RNG ceiling: the reference's two Philox-4x32-10 calls per particle-axis alone
     # run at 3.11e11 draw pairs/s on a B200 (profiles/micro_philox_r01.txt); the
-    # FP32 engine draws one call per particle-axis
-    draws_ps = 3.114e11 * (2.0 if f32 else 1.0)
+    # FP32 engine draws one call per particle-axis and iteration pair (4x fewer)
+    draws_ps = 3.114e11 * (4.0 if f32 else 1.0)
     rng_peak = draws_ps / d * world  # whole job
     roofline["rng_ceiling"] = {"bound": "issue (Philox IMAD.WIDE/LOP3)", "achieved": value,
                                "peak": rng_peak, "unit": "particle-updates/s", "frac": value / rng_peak,
