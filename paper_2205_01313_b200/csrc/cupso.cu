@@ -611,440 +611,7 @@ cupso_status launch_tiled(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   return CUPSO_OK;
 }
 
-// Speculative temporally-blocked mode of cuda-sync (cupso_spec.cuh): each
-// pass keeps every particle in registers for K iterations against a fixed
-// snapshot and is re-run exactly when an admission falsifies it. Available
-// for dims 1/2/4/8 (the particle's state must fit in registers); needs a second
-// state buffer. CUPSO_SYNC_MODE selects another mode; CUPSO_SPEC_K caps K.
-// (particles per thread unit, min blocks/SM) per dims: the whole particle
-// state plus two Philox streams per axis must stay in registers (no spills,
-// ptxas.log); the cos-based fitnesses need a few more.
-template <int F, int D>
-struct SpecKernel {
-  static constexpr int kNP = D == 1 ? 4 : (D == 2 ? 2 : 1);
-  static constexpr int kMinB = D == 8 || D == 1 ? 2 : (F >= kGriewank ? 2 : 3);
-  static const void* fn() { return reinterpret_cast<const void*>(k_spec<F, D, kNP, kMinB>); }
-};
-
-// The speculative kernel chosen for a swarm: function, particles per thread
-// unit, lanes per particle, dynamic SMEM bytes (SMEM-resident lane state).
-struct SpecPick {
-  const void* fn = nullptr;
-  int np = 1, g = 1;
-  size_t smem = 0;
-};
-
-template <int F, int DL, int G, int MINB, bool SM, bool RAGGED = false>
-SpecPick split_pick() {
-  SpecPick k;
-  k.fn = reinterpret_cast<const void*>(k_spec_split<F, DL, G, MINB, SM, RAGGED>);
-  k.g = G;
-  constexpr size_t tw = (sizeof(typename Fit<F>::Term) + 7) / 8;
-  k.smem = SM ? (3ull + (sizeof(typename Fit<F>::Term) >= 8 ? tw : 0)) * DL * kSyncThreads * sizeof(double) : 0;
-  return k;
-}
-template <int F, int NP, int MINB>
-SpecPick d1_pick() {
-  SpecPick k;
-  k.fn = reinterpret_cast<const void*>(k_spec<F, 1, NP, MINB>);
-  k.np = NP;
-  return k;
-}
-
-// Alternative tunings for the BASELINE dims, selected with CUPSO_SPEC_CFG=<n>
-// (exploration; 0 = the default).
-template <int F>
-SpecPick spec_kernel_alt(uint32_t d, int cfg) {
-  if (d == 32) {
-    switch (cfg) {
-      case 1: return split_pick<F, 4, 8, 2, false>();
-      case 2: return split_pick<F, 8, 4, 1, false>();
-      case 3: return split_pick<F, 4, 8, 3, false>();
-      case 4: return split_pick<F, 8, 4, 3, true>();
-      case 5: return split_pick<F, 8, 4, 4, true>();
-      case 6: return split_pick<F, 4, 8, 4, true>();
-      case 7: return split_pick<F, 8, 4, 2, true>();
-      case 8: return split_pick<F, 8, 4, 2, false, true>();
-    }
-  }
-  if (d == 1) {
-    switch (cfg) {
-      case 1: return d1_pick<F, 1, 4>();
-      case 2: return d1_pick<F, 1, 6>();
-      case 3: return d1_pick<F, 2, 4>();
-      case 5: return d1_pick<F, 4, 3>();
-      case 6: return d1_pick<F, 8, 1>();
-    }
-  } else if (d == 8) {
-    SpecPick k;
-    switch (cfg) {
-      case 1: k.fn = reinterpret_cast<const void*>(k_spec<F, 8, 1, 3>); return k;
-      case 2: k.fn = reinterpret_cast<const void*>(k_spec<F, 8, 1, 1>); return k;
-    }
-  }
-  return {};
-}
-
-// The speculative kernel for dims d ({} when d has no instantiation): whole
-// particle per thread in registers for d <= 8, G lanes x 8 axes beyond.
-template <int F>
-SpecPick spec_kernel(uint32_t d, uint32_t n, int nsm) {
-  if (const char* e = getenv("CUPSO_SPEC_CFG")) {
-    const SpecPick k = spec_kernel_alt<F>(d, atoi(e));
-    if (k.fn) return k;
-  }
-  // d = 1 swarms too small to fill the GPU with 4 particles per thread (two
-  // rounds of 2 x 256 resident threads per SM) take one particle per thread:
-  // 2^16 particles run 1.65x faster that way (B200, round 1)
-  if (d == 1 && n < 4u * 2u * 512u * static_cast<uint32_t>(nsm)) return d1_pick<F, 1, 4>();
-  SpecPick k;
-  switch (d) {
-    case 1: k.np = SpecKernel<F, 1>::kNP; k.fn = SpecKernel<F, 1>::fn(); break;
-    case 2: k.np = SpecKernel<F, 2>::kNP; k.fn = SpecKernel<F, 2>::fn(); break;
-    case 4: k.np = SpecKernel<F, 4>::kNP; k.fn = SpecKernel<F, 4>::fn(); break;
-    case 8: k.np = SpecKernel<F, 8>::kNP; k.fn = SpecKernel<F, 8>::fn(); break;
-    case 16: return split_pick<F, 8, 2, 2, false>();
-    case 32: return split_pick<F, 8, 4, 2, false>();
-    case 64: return split_pick<F, 8, 8, 2, false>();
-  }
-  if (k.fn) return k;
-  // any other d up to 256: 8 axis slots per lane, the tail lanes ragged
-  if (d <= 8) return split_pick<F, 8, 1, 2, false, true>();
-  if (d <= 16) return split_pick<F, 8, 2, 2, false, true>();
-  if (d <= 32) return split_pick<F, 8, 4, 2, false, true>();
-  if (d <= 64) return split_pick<F, 8, 8, 2, false, true>();
-  if (d <= 128) return split_pick<F, 8, 16, 2, false, true>();
-  if (d <= 256) return split_pick<F, 8, 32, 2, false, true>();
-  return k;
-}
-
-// Grid of the register-resident pass kernels (grid-stride over thread units).
-// Default: every SM gets the same number of resident blocks (the work per SM
-// then differs by at most one unit per thread). CUPSO_GRID_POLICY=balanced
-// instead equalises units per thread, which can leave SMs with fewer blocks
-// (2^20 d = 1: 256 blocks on 148 SMs -> 13 % idle).
-uint64_t pass_grid(uint64_t units, int per_sm, int nsm) {
-  const uint64_t full = static_cast<uint64_t>(per_sm) * nsm;
-  const uint64_t need = (units + kSyncThreads - 1) / kSyncThreads;
-  const char* e = getenv("CUPSO_GRID_POLICY");
-  if (e && !strcmp(e, "balanced")) {
-    const uint64_t resident = full * kSyncThreads;
-    const uint64_t rounds = (units + resident - 1) / resident;
-    const uint64_t threads = (units + rounds - 1) / rounds;
-    return std::max<uint64_t>(1, (threads + kSyncThreads - 1) / kSyncThreads);
-  }
-  return std::max<uint64_t>(1, std::min(full, need));
-}
-
-// Mailbox [2][n] pass records (double-buffered by exchange parity) followed
-// by n + 1 flag words, zeroed.
-size_t p2p_bytes(const cupso_swarm* h, uint32_t n) {
-  return (2ull * n * spec_rec_bytes(h->P.d) + 15) / 16 * 16 + 4ull * (n + 1);
-}
-uint32_t* p2p_flags(const cupso_swarm* h, unsigned char* buf, uint32_t n) {
-  return reinterpret_cast<uint32_t*>(buf + (2ull * n * spec_rec_bytes(h->P.d) + 15) / 16 * 16);
-}
-
-// A tiny all-gather on the shard's stream, used only during setup.
-bool ipc_allgather(cupso_swarm* h, const void* mine, void* all, size_t bytes) {
-  void *dsend = nullptr, *drecv = nullptr;
-  bool ok = cudaMalloc(&dsend, bytes) == cudaSuccess && cudaMalloc(&drecv, bytes * h->nranks) == cudaSuccess &&
-            cudaMemcpyAsync(dsend, mine, bytes, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
-  ok = ok && nccl().allGather(dsend, drecv, bytes, /*ncclInt8*/ 0, h->comm, h->stream) == 0;
-  ok = ok && cudaMemcpyAsync(all, drecv, bytes * h->nranks, cudaMemcpyDeviceToHost, h->stream) == cudaSuccess;
-  ok = ok && cudaStreamSynchronize(h->stream) == cudaSuccess;
-  if (dsend) cudaFree(dsend);
-  if (drecv) cudaFree(drecv);
-  cudaGetLastError();
-  return ok;
-}
-
-
-// CUDA IPC between shard processes (NCCL ranks, or any host channel through
-// cupso_ipc_handles / cupso_ipc_link): each rank exports its SpecCtl and its
-// pass-record mailbox; opening the peers' gives the early-stop hints
-// (KCtl.peer_tmin) and, with p2p, the pass-record exchange fused into k_spec.
-struct IpcSlot {
-  cudaIpcMemHandle_t ctl, box;
-  int ok, box_ok;
-  int pad[14];
-};
-static_assert(sizeof(IpcSlot) == 192, "IpcSlot is part of the cupso_ipc_handles contract");
-
-void ipc_export(cupso_swarm* h, uint32_t n, bool want_box, IpcSlot* mine) {
-  *mine = IpcSlot{};
-  mine->ok = h->spec_ctl && cudaIpcGetMemHandle(&mine->ctl, h->spec_ctl) == cudaSuccess;
-  if (want_box && !h->p2p_buf) {
-    void* b = nullptr;
-    if (cudaMalloc(&b, p2p_bytes(h, n)) == cudaSuccess && cudaMemset(b, 0, p2p_bytes(h, n)) == cudaSuccess) {
-      h->allocs.push_back(b);
-      h->p2p_buf = static_cast<unsigned char*>(b);
-    }
-  }
-  mine->box_ok = want_box && h->p2p_buf && cudaIpcGetMemHandle(&mine->box, h->p2p_buf) == cudaSuccess;
-  cudaGetLastError();
-}
-
-// Open every peer's exports; returns whether all mailboxes were mapped (the
-// hints are set either way, or cleared on failure). The fused exchange is
-// switched on only by the caller, after every rank agreed.
-bool ipc_open(cupso_swarm* h, const IpcSlot* all, uint32_t n, uint32_t rank, std::vector<unsigned char*>& boxes) {
-  bool ok = true, box_ok = true;
-  for (uint32_t r = 0; r < n; ++r) {
-    ok = ok && all[r].ok;
-    box_ok = box_ok && all[r].box_ok;
-  }
-  uint32_t np = 0;
-  boxes.assign(n, nullptr);
-  for (uint32_t r = 0; ok && r < n; ++r) {
-    if (r == rank) {
-      boxes[r] = h->p2p_buf;
-      continue;
-    }
-    void* base = nullptr;
-    if (cudaIpcOpenMemHandle(&base, all[r].ctl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      ok = false;
-      break;
-    }
-    h->ipc_opened.push_back(base);
-    h->C.peer_tmin[np++] = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(base) + offsetof(SpecCtl, tmin));
-    if (box_ok) {
-      void* bb = nullptr;
-      if (cudaIpcOpenMemHandle(&bb, all[r].box, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        box_ok = false;
-      } else {
-        h->ipc_opened.push_back(bb);
-        boxes[r] = static_cast<unsigned char*>(bb);
-      }
-    }
-  }
-  cudaGetLastError();
-  h->C.npeers = ok ? np : 0;
-  return ok && box_ok;
-}
-
-void p2p_enable(cupso_swarm* h, const std::vector<unsigned char*>& boxes, uint32_t n, uint32_t rank) {
-  for (uint32_t r = 0; r < n; ++r) {
-    h->C.mbox[r] = boxes[r];
-    h->C.flag[r] = p2p_flags(h, boxes[r], n);
-  }
-  h->C.p2p_n = n;
-  h->C.p2p_rank = rank;
-  h->p2p = true;
-}
-
-// NCCL shards: the same, collectively at the first speculative step (two
-// all-gathers: the IPC exports, then whether every rank mapped every peer --
-// the exchange mode must agree across ranks). Any failure leaves the hints off
-// and the NCCL exchange in place. CUPSO_SPEC_PEERS=0 disables both,
-// CUPSO_SPEC_EXCHANGE=p2p opts into the fused exchange.
-void link_ipc_peers(cupso_swarm* h) {
-  h->C.npeers = 0;
-  const char* e = getenv("CUPSO_SPEC_PEERS");
-  const char* x = getenv("CUPSO_SPEC_EXCHANGE");
-  const uint32_t n = static_cast<uint32_t>(h->nranks);
-  const bool want = !(e && !strcmp(e, "0")) && n > 1 && n <= 16;
-  const bool want_p2p = want && x && !strcmp(x, "p2p");
-  IpcSlot mine{};
-  if (want) ipc_export(h, n, want_p2p, &mine);
-  // the all-gathers run on every rank whatever it decided, so collectives stay matched
-  std::vector<IpcSlot> all(n);
-  if (!ipc_allgather(h, &mine, all.data(), sizeof(IpcSlot))) return;
-  std::vector<unsigned char*> boxes;
-  const bool box_ok = want && ipc_open(h, all.data(), n, static_cast<uint32_t>(h->rank), boxes);
-  if (!want_p2p) return;
-  int mine_ok = box_ok ? 1 : 0;
-  std::vector<int> oks(n, 0);
-  bool agree = ipc_allgather(h, &mine_ok, oks.data(), sizeof(int));
-  for (uint32_t r = 0; agree && r < n; ++r) agree = oks[r] != 0;
-  if (agree) p2p_enable(h, boxes, n, static_cast<uint32_t>(h->rank));
-}
-
-bool spec_fits(cupso_swarm* h) {
-  if (h->spec_checked) return h->spec_grid > 0;
-  h->spec_checked = true;
-  if (!h->P.scaled_ok) return false;  // vel_step53 would not be exact
-  if (const char* e = getenv("CUPSO_SYNC_MODE"))
-    if (strcmp(e, "spec") != 0 && strcmp(e, "auto") != 0) return false;
-  SpecPick k;
-  dispatch_fit(h->fid, [&](auto F) { k = spec_kernel<decltype(F)::value>(h->P.d, h->P.n, num_sms(h->device)); });
-  if (!k.fn) return false;
-  const int np = k.np, g = k.g;
-  int per_sm = 0;
-  if ((k.smem && cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(k.smem)) != cudaSuccess) ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kSyncThreads, k.smem) != cudaSuccess ||
-      per_sm < 1) {
-    cudaGetLastError();
-    return false;
-  }
-  h->spec_smem = k.smem;
-  const uint64_t units = (h->P.n + np - 1ull) / np * g;  // g lanes per unit
-  const uint64_t grid = pass_grid(units, per_sm, num_sms(h->device));
-  // second state buffer (the pass writes B while A stays intact for a re-run)
-  const size_t cells = h->P.ld * h->P.d;
-  void *pos = nullptr, *vel = nullptr, *pb = nullptr, *pbf = nullptr, *ctl = nullptr, *host = nullptr;
-  void *rl = nullptr, *ra = nullptr;
-  const size_t rb = spec_rec_bytes(h->P.d);
-  if (cudaMalloc(&pos, cells * 8) != cudaSuccess || cudaMalloc(&vel, cells * 8) != cudaSuccess ||
-      cudaMalloc(&pb, cells * 8) != cudaSuccess || cudaMalloc(&pbf, h->P.ld * 8) != cudaSuccess ||
-      cudaMalloc(&ctl, sizeof(SpecCtl)) != cudaSuccess || cudaMalloc(&rl, rb) != cudaSuccess ||
-      cudaMalloc(&ra, rb * std::max(1, h->nranks)) != cudaSuccess ||
-      (!h->spec_host && cudaMallocHost(&host, sizeof(SpecCtl)) != cudaSuccess)) {
-    for (void* p : {pos, vel, pb, pbf, ctl, rl, ra}) cudaFree(p);
-    if (host) cudaFreeHost(host);
-    cudaGetLastError();
-    return false;  // not enough HBM for two copies: another mode runs
-  }
-  for (void* p : {pos, vel, pb, pbf, ctl, rl, ra}) h->allocs.push_back(p);
-  h->spec_rec_local = static_cast<unsigned char*>(rl);
-  h->spec_rec_all = static_cast<unsigned char*>(ra);
-  h->S_alt = KState{static_cast<double*>(pos), static_cast<double*>(vel), static_cast<double*>(pb),
-                    static_cast<double*>(pbf)};
-  h->spec_ctl = static_cast<SpecCtl*>(ctl);
-  if (host) h->spec_host = static_cast<SpecCtl*>(host);
-  if (ensure_queue(h, grid) != CUPSO_OK) return false;
-  const char* ke = getenv("CUPSO_SPEC_K");
-  h->spec_kmax = ke ? std::max(1, atoi(ke)) : 64;
-  h->spec_grid = static_cast<int>(grid);
-  if (h->comm) link_ipc_peers(h);
-  return true;
-}
-
-// The all-gather of one record per shard: NCCL on the stream, or the
-// caller's host callback (cupso_step_exchange). Returns the device buffer of
-// the gathered records in *all.
-cupso_status exchange(cupso_swarm* h, const unsigned char* local_dev, size_t bytes, unsigned char** all) {
-  if (h->comm) {
-    const int r = nccl().allGather(local_dev, h->spec_rec_all, bytes, /*ncclInt8*/ 0, h->comm, h->stream);
-    if (r != 0)
-      return fail(CUPSO_ERUNTIME, "ncclAllGather failed: %s", nccl().getErrorString ? nccl().getErrorString(r) : "?");
-    *all = h->spec_rec_all;
-    return CUPSO_OK;
-  }
-  const size_t need = bytes * h->xranks;
-  if (h->xrec_cap < need) {
-    void* p;
-    TRY(dmalloc(h, &p, need));
-    h->xrec_dev = static_cast<unsigned char*>(p);
-    h->xrec_cap = need;
-  }
-  h->xlocal.resize(bytes);
-  h->xall.resize(need);
-  CK(cudaMemcpyAsync(h->xlocal.data(), local_dev, bytes, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  if (h->xfn(h->xlocal.data(), h->xall.data(), bytes, h->xuser) != 0)
-    return fail(CUPSO_ERUNTIME, "exchange callback failed");
-  CK(cudaMemcpyAsync(h->xrec_dev, h->xall.data(), need, cudaMemcpyHostToDevice, h->stream));
-  *all = h->xrec_dev;
-  return CUPSO_OK;
-}
-
-cupso_status spec_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
-  SpecCtl& c = *h->spec_host;
-  c = SpecCtl{t0, 1u, 0u, 1u, ~0u, 0u, 0u, 0u};
-  CK(cudaMemcpyAsync(h->spec_ctl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemsetAsync(h->C.q_count, 0, 3 * sizeof(uint32_t), h->stream));
-  SpecPick k;
-  dispatch_fit(h->fid, [&](auto F) { k = spec_kernel<decltype(F)::value>(h->P.d, h->P.n, num_sms(h->device)); });
-  const void* kfn = k.fn;
-  const uint32_t kmax = h->spec_kmax;
-  KState s0 = h->S, s1 = h->S_alt;
-  int sharded = h->comm != nullptr || h->xfn != nullptr || h->p2p;
-  const uint32_t nrec = h->comm ? static_cast<uint32_t>(h->nranks) : h->xranks;
-  unsigned char* rec = h->spec_rec_local;
-  void* args[] = {&h->P, &s0, &s1, &h->C, &h->spec_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec, &sharded};
-  const size_t rb = spec_rec_bytes(h->P.d);
-  const bool trace_passes = getenv("CUPSO_SPEC_TRACE") != nullptr;  // exploration: one line per pass
-  for (;;) {
-    // passes still needed if no speculation fails from here on
-    uint32_t n = 0, t = c.t0, K = c.K, ks = c.kspec;
-    if (trace_passes) n = 1, t = t1;  // one pass at a time, synchronised
-    while (t < t1) {
-      t += K;
-      ++n;
-      if (K >= ks) ks = std::min(2 * ks, kmax);
-      K = std::min(ks, t1 - t);
-    }
-    for (uint32_t i = 0; i < n; ++i) {
-      CK(cudaLaunchKernel(kfn, dim3(h->spec_grid), dim3(kSyncThreads), args, h->spec_smem, h->stream));
-      if (sharded && !h->p2p) {  // one exchange per pass: the shards' records, then the same decision everywhere
-        unsigned char* all = nullptr;
-        TRY(exchange(h, h->spec_rec_local, rb, &all));
-        k_spec_commit<<<1, 256, 0, h->stream>>>(h->P, h->C, h->spec_ctl, all, nrec, t1, kmax);
-        CK(cudaGetLastError());
-      }
-    }
-    h->spec_launches += n;
-    const SpecCtl before = c;
-    CK(cudaMemcpyAsync(&c, h->spec_ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    if (trace_passes)
-      fprintf(stderr, "spec pass t0=%u K=%u -> %s (next t0=%u K=%u)\n", before.t0, before.K,
-              c.fails > before.fails ? "FALSIFIED" : "committed", c.t0, c.K);
-    if (c.t0 >= t1) break;
-  }
-  h->spec_passes += c.passes;
-  h->spec_fails += c.fails;
-  if (c.parity) {  // the committed state ended in the second buffer
-    std::swap(h->S, h->S_alt);
-    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
-    h->graphs.clear();  // captured graphs hold the old state pointers
-  }
-  return CUPSO_OK;
-}
-
-// Register-resident mode of cuda-async (k_async_reg): dims 1/2/4/8, each
-// thread runs K iterations on its particles in registers. CUPSO_ASYNC_MODE=
-// reg|tiled|plain selects; CUPSO_ASYNC_K sets K (default 32).
-template <int F, int D>
-const void* async_reg_kernel() {
-  return reinterpret_cast<const void*>(
-      k_async_reg<F, D, SpecKernel<F, D>::kNP, SpecKernel<F, D>::kMinB>);
-}
-template <int F>
-const void* async_reg_kernel(uint32_t d, int* np) {
-  switch (d) {
-    case 1: *np = SpecKernel<F, 1>::kNP; return async_reg_kernel<F, 1>();
-    case 2: *np = SpecKernel<F, 2>::kNP; return async_reg_kernel<F, 2>();
-    case 4: *np = SpecKernel<F, 4>::kNP; return async_reg_kernel<F, 4>();
-    case 8: *np = SpecKernel<F, 8>::kNP; return async_reg_kernel<F, 8>();
-    default: return nullptr;
-  }
-}
-
-bool async_reg_fits(cupso_swarm* h) {
-  if (h->areg_checked) return h->areg_grid > 0;
-  h->areg_checked = true;
-  if (!h->P.scaled_ok) return false;
-  const char* mode = getenv("CUPSO_ASYNC_MODE");
-  if (mode && strcmp(mode, "reg") != 0 && strcmp(mode, "auto") != 0) return false;
-  const void* kfn = nullptr;
-  int np = 1;
-  dispatch_fit(h->fid, [&](auto F) { kfn = async_reg_kernel<decltype(F)::value>(h->P.d, &np); });
-  if (!kfn) return false;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kSyncThreads, 0) != cudaSuccess || per_sm < 1) {
-    cudaGetLastError();
-    return false;
-  }
-  const uint64_t units = (h->P.n + np - 1ull) / np;
-  h->areg_grid = static_cast<int>(pass_grid(units, per_sm, num_sms(h->device)));
-  const char* k = getenv("CUPSO_ASYNC_K");
-  h->areg_k = k ? std::max(1, atoi(k)) : 32;
-  return true;
-}
-
-cupso_status launch_async_reg(cupso_swarm* h, uint32_t t0, uint32_t t1) {
-  CK(cudaMemsetAsync(h->C.seq, 0, sizeof(uint32_t), h->stream));
-  const void* kfn = nullptr;
-  int np = 1;
-  dispatch_fit(h->fid, [&](auto F) { kfn = async_reg_kernel<decltype(F)::value>(h->P.d, &np); });
-  uint32_t K = static_cast<uint32_t>(h->areg_k);
-  void* args[] = {&h->P, &h->S, &h->C, &t0, &t1, &K};
-  CK(cudaLaunchKernel(kfn, dim3(h->areg_grid), dim3(kSyncThreads), args, 0, h->stream));
-  return CUPSO_OK;
-}
+#include "cupso_spec_host.inc"
 
 cupso_status launch_persistent(cupso_swarm* h, int variant, uint32_t t0, uint32_t t1) {
   if (variant == CUPSO_SYNC && resident_fits(h)) return launch_resident(h, t0, t1);
@@ -1117,122 +684,7 @@ cupso_status sharded_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
   return CUPSO_OK;
 }
 
-// ----------------------------------------------------------- FP32 engine
-template <int F, int D>
-const void* f32_kernel(int* np) {
-  constexpr int NP = D <= 2 ? 4 : (D == 4 ? 2 : 1);
-  *np = NP;
-  return reinterpret_cast<const void*>(k_spec32<F, D, NP, D == 8 ? 2 : 3>);
-}
-
-cupso_status ensure_f32(cupso_swarm* h) {
-  if (h->f32_ready) return CUPSO_OK;
-  const size_t cells = h->P.ld * h->P.d;
-  void* p[8];
-  for (int k = 0; k < 2; ++k) {
-    TRY(dmalloc(h, &p[4 * k + 0], cells * 4));
-    TRY(dmalloc(h, &p[4 * k + 1], cells * 4));
-    TRY(dmalloc(h, &p[4 * k + 2], cells * 4));
-    TRY(dmalloc(h, &p[4 * k + 3], h->P.ld * 4));
-  }
-  h->S32 = KState32{static_cast<float*>(p[0]), static_cast<float*>(p[1]), static_cast<float*>(p[2]),
-                    static_cast<float*>(p[3])};
-  h->S32_alt = KState32{static_cast<float*>(p[4]), static_cast<float*>(p[5]), static_cast<float*>(p[6]),
-                        static_cast<float*>(p[7])};
-  void* c;
-  TRY(dmalloc(h, &c, sizeof(SpecCtl32)));
-  CK(cudaMemset(c, 0, sizeof(SpecCtl32)));
-  h->spec32_ctl = static_cast<SpecCtl32*>(c);
-  if (!h->spec_rec_local) {
-    void* rl;
-    TRY(dmalloc(h, &rl, spec_rec_bytes(h->P.d)));
-    h->spec_rec_local = static_cast<unsigned char*>(rl);
-  }
-  const KParams& P = h->P;
-  h->Q = KParams32{static_cast<float>(P.w), static_cast<float>(P.c1), static_cast<float>(P.c2),
-                   static_cast<float>(P.min_pos), static_cast<float>(P.max_pos), static_cast<float>(P.min_v),
-                   static_cast<float>(P.max_v)};
-  int np = 1;
-  dispatch_fit(h->fid, [&](auto F) {
-    constexpr int f = decltype(F)::value;
-    switch (h->P.d) {
-      case 1: h->f32_kfn = f32_kernel<f, 1>(&np); break;
-      case 2: h->f32_kfn = f32_kernel<f, 2>(&np); break;
-      case 4: h->f32_kfn = f32_kernel<f, 4>(&np); break;
-      case 8: h->f32_kfn = f32_kernel<f, 8>(&np); break;
-      default: h->f32_kfn = nullptr;  // any other dims: k_wave32, one launch per iteration
-    }
-  });
-  if (h->f32_kfn) {
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->f32_kfn, kSyncThreads, 0));
-    if (per_sm < 1) return fail(CUPSO_ECUDA, "cuda-sync-f32: kernel cannot be resident");
-    const uint64_t units = (h->P.n + np - 1ull) / np;
-    h->f32_grid = static_cast<int>(pass_grid(units, per_sm, num_sms(h->device)));
-  } else {
-    h->f32_grid = static_cast<int>(std::min<uint64_t>((h->P.n + kSyncThreads - 1) / kSyncThreads,
-                                                     static_cast<uint64_t>(num_sms(h->device)) * 8));
-  }
-  h->f32_ready = true;
-  return CUPSO_OK;
-}
-
-int conv_blocks(const cupso_swarm* h) {
-  return static_cast<int>(std::min<uint64_t>((h->P.ld * h->P.d + 255) / 256, 148ull * 16));
-}
-
-// FP32 copy newer than the FP64 state: convert back (any FP64 consumer calls this).
-cupso_status sync_f64(cupso_swarm* h) {
-  if (!h->f32_active) return CUPSO_OK;
-  CK(cudaSetDevice(h->device));
-  k_to_f64<<<conv_blocks(h), 256, 0, h->stream>>>(h->P, h->S32, h->S);
-  CK(cudaGetLastError());
-  h->f32_active = false;
-  return CUPSO_OK;
-}
-
-cupso_status f32_steps(cupso_swarm* h, uint32_t t0, uint32_t t1) {
-  if (!h->f32_kfn) {  // generic dims: one k_wave32 launch per iteration
-    cudaError_t e = cudaSuccess;
-    dispatch_fit(h->fid, [&](auto F) {
-      constexpr int f = decltype(F)::value;
-      for (uint32_t t = t0; t < t1 && e == cudaSuccess; ++t) {
-        k_wave32<f><<<h->f32_grid, kSyncThreads, h->P.d * sizeof(float), h->stream>>>(h->P, h->Q, h->S32, h->C,
-                                                                                      h->spec32_ctl, t);
-        e = cudaGetLastError();
-      }
-    });
-    CK(e);
-    return CUPSO_OK;
-  }
-  SpecCtl& c = *h->spec_host;
-  c = SpecCtl{t0, 1u, 0u, 1u, ~0u, 0u, 0u, 0u};
-  CK(cudaMemcpyAsync(&h->spec32_ctl->ctl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemsetAsync(&h->spec32_ctl->key, 0, sizeof(unsigned long long), h->stream));
-  const uint32_t kmax = h->spec_kmax;
-  KState32 s0 = h->S32, s1 = h->S32_alt;
-  unsigned char* rec = h->spec_rec_local;
-  void* args[] = {&h->P, &h->Q, &s0, &s1, &h->C, &h->spec32_ctl, &t1, const_cast<uint32_t*>(&kmax), &rec};
-  for (;;) {
-    uint32_t n = 0, t = c.t0, K = c.K, ks = c.kspec;
-    while (t < t1) {
-      t += K;
-      ++n;
-      if (K >= ks) ks = std::min(2 * ks, kmax);
-      K = std::min(ks, t1 - t);
-    }
-    for (uint32_t i = 0; i < n; ++i)
-      CK(cudaLaunchKernel(h->f32_kfn, dim3(h->f32_grid), dim3(kSyncThreads), args, 0, h->stream));
-    h->spec_launches += n;
-    CK(cudaMemcpyAsync(&c, &h->spec32_ctl->ctl, sizeof c, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    if (c.t0 >= t1) break;
-  }
-  h->spec_passes += c.passes;
-  h->spec_fails += c.fails;
-  if (c.parity) std::swap(h->S32, h->S32_alt);
-  return CUPSO_OK;
-}
+#include "cupso_f32_host.inc"
 
 cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* seconds) {
   if (!h) return fail(CUPSO_EINVAL, "null swarm handle");
