@@ -46,12 +46,14 @@ struct Fit32<kCubic> {
     acc += __fmaf_rn(__fmaf_rn(v - 0.8f, v, -1000.f), v, 8000.f);
   }
   __device__ __forceinline__ float value() const { return acc; }
+  __device__ __forceinline__ void merge_xor(int off, int w) { acc += __shfl_xor_sync(0xffffffffu, acc, off, w); }
 };
 template <>
 struct Fit32<kSphere> {
   float acc = 0.f;
   __device__ __forceinline__ void add(float v, uint32_t) { acc = __fmaf_rn(v, v, acc); }
   __device__ __forceinline__ float value() const { return -acc; }
+  __device__ __forceinline__ void merge_xor(int off, int w) { acc += __shfl_xor_sync(0xffffffffu, acc, off, w); }
 };
 template <>
 struct Fit32<kRosenbrock> {
@@ -65,6 +67,7 @@ struct Fit32<kRosenbrock> {
     prev = v;
   }
   __device__ __forceinline__ float value() const { return -acc; }
+  __device__ __forceinline__ void merge_xor(int off, int w) { acc += __shfl_xor_sync(0xffffffffu, acc, off, w); }
 };
 template <>
 struct Fit32<kGriewank> {
@@ -74,6 +77,10 @@ struct Fit32<kGriewank> {
     prod *= cosf(v * rsqrtf(static_cast<float>(axis + 1)));
   }
   __device__ __forceinline__ float value() const { return -((1.f + sum) - prod); }
+  __device__ __forceinline__ void merge_xor(int off, int w) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, off, w);
+    prod *= __shfl_xor_sync(0xffffffffu, prod, off, w);
+  }
 };
 template <>
 struct Fit32<kRastrigin> {
@@ -82,6 +89,7 @@ struct Fit32<kRastrigin> {
     acc += __fmaf_rn(v, v, __fmaf_rn(-10.f, cospif(2.f * v), 10.f));
   }
   __device__ __forceinline__ float value() const { return -acc; }
+  __device__ __forceinline__ void merge_xor(int off, int w) { acc += __shfl_xor_sync(0xffffffffu, acc, off, w); }
 };
 
 // Packed (fitness, particle) key: u64 max == beats() order.
@@ -149,6 +157,57 @@ struct SpecCtl32 {
   SpecCtl ctl;
   unsigned long long key;  // best (fit, particle) admitted at the pass's last iteration
 };
+
+// Pass tail shared by the FP32 pass kernels.
+__device__ __forceinline__ void spec32_finish(const KParams& P, const KState32& So, const KCtl& C, SpecCtl32* sc32,
+                                              unsigned long long& s_key, unsigned long long& s_adm, int& s_last,
+                                              uint32_t t_end, uint32_t kmax, unsigned char* rec_out, uint32_t tl,
+                                              unsigned long long bkey, uint32_t adm) {
+  SpecCtl* sc = &sc32->ctl;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const size_t ld = P.ld;
+  // ---- aggregation: warp shuffle max of the packed key, one SMEM atomicMax
+  // per warp, one global atomicMax per block (the paper's atomic scheme)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, bkey, off);
+    bkey = o > bkey ? o : bkey;
+  }
+  const uint32_t wadm = __reduce_add_sync(0xffffffffu, adm);
+  if (lane == 0) {
+    if (bkey) atomicMax(&s_key, bkey);
+    if (wadm) atomicAdd(&s_adm, static_cast<unsigned long long>(wadm));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (s_key) atomicMax(&sc32->key, s_key);
+    if (s_adm) atomicAdd(&C.admitted[tl], s_adm);
+    __threadfence();
+    s_last = last_block_done(C);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last block: the pass record, then the shared decision (spec_decide)
+  __threadfence();
+  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(&sc32->key);
+  SpecRec* rec = reinterpret_cast<SpecRec*>(rec_out);
+  double* rpos = reinterpret_cast<double*>(rec_out + sizeof(SpecRec));
+  const uint32_t wi = key ? key_idx(key) : kNoParticle;
+  for (uint32_t a = tid; a < P.d; a += blockDim.x)
+    rpos[a] = key ? static_cast<double>(__ldcg(&So.pos[static_cast<size_t>(a) * ld + (wi - P.base)])) : 0.0;
+  if (tid == 0) {
+    rec->tmin = ld_volatile_u32(&sc->tmin);
+    rec->admitted = static_cast<uint32_t>(__ldcg(&C.admitted[tl]));
+    rec->fit = key ? static_cast<double>(key_fit(key)) : -INFINITY;
+    rec->particle = wi;
+    rec->pad = 0;
+    C.admitted[tl] = 0;
+    sc32->key = 0;
+    __threadfence();
+  }
+  __syncthreads();
+  spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
+}
 
 template <int F, int D, int NP, int MINB>
 __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParams32 Q, KState32 S0, KState32 S1,
@@ -287,47 +346,138 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParam
       }
     }
   }
-  // ---- aggregation: warp shuffle max of the packed key, one SMEM atomicMax
-  // per warp, one global atomicMax per block (the paper's atomic scheme)
+  spec32_finish(P, So, C, sc32, s_key, s_adm, s_last, t_end, kmax, rec_out, tl, bkey, adm);
+}
+
+// Wide FP32 swarms (d > 8, up to 256): G lanes per particle, 8 axis slots each
+// (the last lane group ragged when d < 8 G), as k_spec_split -- but the FP32
+// engine is statistical, so the lanes' partial fitnesses combine by a
+// butterfly (shfl_xor) instead of the FP64 kernels' ordered fold.
+template <int F, int DL, int G, int MINB>
+__global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32_split(KParams P, KParams32 Q, KState32 S0, KState32 S1,
+                                                                    KCtl C, SpecCtl32* sc32, uint32_t t_end,
+                                                                    uint32_t kmax, unsigned char* rec_out) {
+  static_assert(32 % G == 0, "G must divide the warp");
+  __shared__ float s_gpos[DL * G];
+  __shared__ unsigned long long s_key, s_adm;
+  __shared__ uint32_t s_ctl[4];
+  __shared__ int s_last;
+  SpecCtl* sc = &sc32->ctl;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, sub = lane % G, a0 = sub * DL;
+  if (tid == 0) {
+    s_ctl[0] = ld_volatile_u32(&sc->t0);
+    s_ctl[1] = ld_volatile_u32(&sc->K);
+    s_ctl[2] = ld_volatile_u32(&sc->parity);
+    s_ctl[3] = ld_volatile_u32(&sc->kspec);
+    s_key = 0;
+    s_adm = 0;
+  }
+  for (uint32_t a = tid; a < DL * G; a += blockDim.x) s_gpos[a] = a < P.d ? static_cast<float>(C.snap_pos[a]) : 0.f;
+  __syncthreads();
+  const uint32_t t0 = s_ctl[0], K = s_ctl[1], par = s_ctl[2];
+  if (t0 >= t_end) return;
+  const bool inplace = K == 1;
+  const KState32 Si = par ? S1 : S0;
+  const KState32 So = inplace ? Si : (par ? S0 : S1);
+  const float snap_fit = static_cast<float>(C.snap->fit);
+  const uint32_t tl = t0 + K - 1;
+  auto valid = [&](int a) { return a0 + a < P.d; };
+  unsigned long long bkey = 0;
+  uint32_t adm = 0;
+  uint32_t tstop = warp_tmin(&sc->tmin);
+  const uint32_t stride = gridDim.x * (blockDim.x / G);
+  const size_t ld = P.ld;
+  for (uint32_t u0 = (blockIdx.x * blockDim.x + (tid & ~31u)) / G; u0 < P.n; u0 += stride) {  // warp-uniform
+    tstop = min(tstop, warp_tmin(&sc->tmin));
+    uint32_t te = min(t0 + K, tstop);
+    if (te <= t0) break;
+    const uint32_t li = u0 + lane / G;
+    const bool live = li < P.n;
+    const uint32_t gi = P.base + li;
+    float x[DL], v[DL], pb[DL], pbf = -INFINITY;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const unsigned long long o = __shfl_xor_sync(0xffffffffu, bkey, off);
-    bkey = o > bkey ? o : bkey;
+    for (int a = 0; a < DL; ++a) {
+      x[a] = v[a] = pb[a] = 0.f;
+      if (live && valid(a)) {
+        const size_t at = static_cast<size_t>(a0 + a) * ld + li;
+        x[a] = Si.pos[at];
+        v[a] = Si.vel[at];
+        pb[a] = Si.pb[at];
+      }
+    }
+    if (live) pbf = Si.pbf[li];
+    uint32_t t = t0;
+    bool bad = false, dirty = false;
+    uint32_t odd_w[DL][2];
+    for (; t < te; ++t) {
+      const bool fresh = !(t & 1u) || t == t0;
+#pragma unroll
+      for (int a = 0; a < DL; ++a) {
+        if (!valid(a)) continue;
+        float r1, r2;
+        if (fresh) {
+          uint32_t w0, w1;
+          philox_pair(P, t, gi, a0 + a, w0, w1, odd_w[a][0], odd_w[a][1]);
+          r1 = u24((t & 1u) ? odd_w[a][0] : w0);
+          r2 = u24((t & 1u) ? odd_w[a][1] : w1);
+        } else {
+          r1 = u24(odd_w[a][0]);
+          r2 = u24(odd_w[a][1]);
+        }
+        const float xv = x[a];
+        float nv = __fmaf_rn(Q.c2 * r2, s_gpos[a0 + a] - xv, __fmaf_rn(Q.c1 * r1, pb[a] - xv, Q.w * v[a]));
+        nv = fminf(fmaxf(nv, Q.min_v), Q.max_v);
+        v[a] = nv;
+        x[a] = fminf(fmaxf(xv + nv, Q.min_pos), Q.max_pos);
+      }
+      Fit32<F> acc;
+      if constexpr (F == kRosenbrock) acc.prev = __shfl_up_sync(0xffffffffu, x[DL - 1], 1, G);  // left lane's last axis
+#pragma unroll
+      for (int a = 0; a < DL; ++a)
+        if (valid(a)) acc.add(x[a], a0 + a);
+#pragma unroll
+      for (int off = 1; off < G; off <<= 1) acc.merge_xor(off, G);
+      const float f = acc.value();
+      if (live && f > pbf) {
+        dirty = true;
+        pbf = f;
+#pragma unroll
+        for (int a = 0; a < DL; ++a) pb[a] = x[a];
+      }
+      bool early = false;
+      if (live && f > snap_fit) {
+        if (t < tl) {
+          early = true;
+        } else if (sub == 0) {
+          ++adm;
+          const unsigned long long kk = key32(f, gi);
+          bkey = kk > bkey ? kk : bkey;
+        }
+      }
+      if (__any_sync(0xffffffffu, early)) {
+        if (lane == 0) atomicMin(&sc->tmin, t);
+        tstop = t;
+        bad = true;
+        break;
+      }
+      if (((t - t0) & 15u) == 15u) {
+        tstop = min(tstop, warp_tmin(&sc->tmin));
+        te = min(te, tstop);
+      }
+    }
+    if (!bad && t == t0 + K && live) {
+#pragma unroll
+      for (int a = 0; a < DL; ++a) {
+        if (!valid(a)) continue;
+        const size_t at = static_cast<size_t>(a0 + a) * ld + li;
+        So.pos[at] = x[a];
+        So.vel[at] = v[a];
+        if (!inplace || dirty) So.pb[at] = pb[a];
+      }
+      if (sub == 0 && (!inplace || dirty)) So.pbf[li] = pbf;
+    }
   }
-  const uint32_t wadm = __reduce_add_sync(0xffffffffu, adm);
-  if (lane == 0) {
-    if (bkey) atomicMax(&s_key, bkey);
-    if (wadm) atomicAdd(&s_adm, static_cast<unsigned long long>(wadm));
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (s_key) atomicMax(&sc32->key, s_key);
-    if (s_adm) atomicAdd(&C.admitted[tl], s_adm);
-    __threadfence();
-    s_last = last_block_done(C);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  // ---- last block: the pass record, then the shared decision (spec_decide)
-  __threadfence();
-  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(&sc32->key);
-  SpecRec* rec = reinterpret_cast<SpecRec*>(rec_out);
-  double* rpos = reinterpret_cast<double*>(rec_out + sizeof(SpecRec));
-  const uint32_t wi = key ? key_idx(key) : kNoParticle;
-  for (uint32_t a = tid; a < D; a += blockDim.x)
-    rpos[a] = key ? static_cast<double>(__ldcg(&So.pos[static_cast<size_t>(a) * ld + (wi - P.base)])) : 0.0;
-  if (tid == 0) {
-    rec->tmin = ld_volatile_u32(&sc->tmin);
-    rec->admitted = static_cast<uint32_t>(__ldcg(&C.admitted[tl]));
-    rec->fit = key ? static_cast<double>(key_fit(key)) : -INFINITY;
-    rec->particle = wi;
-    rec->pad = 0;
-    C.admitted[tl] = 0;
-    sc32->key = 0;
-    __threadfence();
-  }
-  __syncthreads();
-  spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
+  spec32_finish(P, So, C, sc32, s_key, s_adm, s_last, t_end, kmax, rec_out, tl, bkey, adm);
 }
 
 // Any dims: one launch per iteration, one particle per thread, state in HBM

@@ -402,6 +402,14 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
 }
 
 // ------------------------------------------------ k_spec for wide swarms
+// tmin as one value for the whole warp (loop bounds of the split kernels must
+// stay warp-uniform: their lanes meet in shuffles every iteration).
+__device__ __forceinline__ uint32_t warp_tmin(const uint32_t* tmin) {
+  uint32_t m = 0;
+  if ((threadIdx.x & 31u) == 0) m = ld_relaxed_gpu(tmin);
+  return __shfl_sync(0xffffffffu, m, 0);
+}
+
 // d = DL * G: a particle is owned by G consecutive lanes, lane s of the group
 // holding axes [s*DL, s*DL + DL) in registers (cfg4: d = 32 = 8 x 4). Per
 // iteration every lane computes its axes' Philox draws, kinematics and
@@ -457,13 +465,13 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
   // its 8 doubles in registers cost spills (cfg4: 2.7 % slower)
   double bf = -INFINITY;
   uint32_t bi = kNoParticle, adm = 0;
-  uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
+  uint32_t tstop = warp_tmin(&sc->tmin);
   const uint32_t per_warp = 32 / G;
   const uint32_t stride = gridDim.x * (blockDim.x / G);
   const size_t ld = P.ld;
   // warp-uniform particle loop: particle = u0 + lane / G
   for (uint32_t u0 = (blockIdx.x * blockDim.x + (tid & ~31u)) / G; u0 < P.n; u0 += stride) {
-    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+    tstop = min(tstop, warp_tmin(&sc->tmin));
     uint32_t te = min(t0 + K, tstop);
     if (te <= t0) break;  // warp-uniform: one load serves the warp
     const uint32_t li = u0 + lane / G;
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
         break;
       }
       if (((t - t0) & 15u) == 15u) {
-        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+        tstop = min(tstop, warp_tmin(&sc->tmin));
         te = min(te, tstop);
       }
     }

@@ -23,10 +23,12 @@ def test_f32_statistics_32_seeds(cupso):
 
 
 @pytest.mark.parametrize("fit,d", [("cubic", 1), ("sphere", 8), ("rastrigin", 2), ("rosenbrock", 4),
-                                   ("griewank", 3), ("sphere", 5)])
+                                   ("griewank", 3), ("sphere", 5), ("rastrigin", 32), ("rosenbrock", 17),
+                                   ("griewank", 100), ("cubic", 256), ("sphere", 300)])
 def test_f32_invariants(cupso, oracle, fit, d):
     """Monotone trace; the record is a consistent (fit, pos) pair of an FP32
-    particle; gbest = max pbest; state in the box. d = 3 / 5 run k_wave32."""
+    particle; gbest = max pbest; state in the box. d = 3 / 5 / 17 / 32 / 100 /
+    256 run k_spec32_split (ragged but for 32), d = 300 k_wave32."""
     f = cupso.find_fitness(fit)
     n, T = 5001, 90
     p = cupso.make_params(f, n, d, T)
@@ -69,3 +71,26 @@ def test_f32_then_fp64_engines(cupso):
         st = sw.state()
         gb = sw.gbest()
     assert (np.diff(tr) >= 0).all() and gb.fit == st.pbest_fit.max()
+
+
+@pytest.mark.parametrize("fit,d", [("rastrigin", 32), ("rosenbrock", 17)])
+def test_f32_wide_statistics(cupso, fit, d):
+    """The split FP32 kernel (lanes' partial fitnesses combined by a butterfly)
+    optimises like the FP64 engine: median final fitness over 12 seeds."""
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, 8192, d, 200)
+    sync = np.array([cupso.find_engine("cuda-sync").run(p, f, cupso.rng_key(s)).gbest_fit for s in range(1, 13)])
+    f32 = np.array([cupso.find_engine("cuda-sync-f32").run(p, f, cupso.rng_key(s)).gbest_fit for s in range(1, 13)])
+    med_s, med_f = np.median(-sync), np.median(-f32)
+    assert med_f < 1.5 * med_s, (med_f, med_s)
+
+
+def test_f32_wide_uses_pass_kernel(cupso):
+    """d = 32 runs register-resident passes (a handful of launches for 256
+    iterations), not one k_wave32 launch per iteration."""
+    f = cupso.find_fitness("rastrigin")
+    p = cupso.make_params(f, 1 << 16, 32, 256)
+    with cupso.Swarm(p, f, 1) as sw:
+        sw.step(cupso.SYNC_F32, 256)
+        passes, fails, launches = sw.spec_stats()
+    assert 0 < launches < 128, (passes, fails, launches)
