@@ -18,6 +18,7 @@ run cfg2_reduction_step k_classic_step 5 1 "X=1" cuda-reduction cubic 20 1 10
 run cfg2_reduction_fold k_classic_fold 5 1 "X=1" cuda-reduction cubic 20 1 10
 run cfg3_async k_async_reg 0 1 "X=1" cuda-async cubic 24 1 100
 run cfg4_spec k_spec 0 60 "CUPSO_SYNC_MODE=spec" cuda-sync rastrigin 20 32 60
+run cfg4_f32 k_spec32_split 0 60 "X=1" cuda-sync-f32 rastrigin 20 32 60
 run cfg4_wave k_wave 5 1 "CUPSO_SYNC_MODE=wave" cuda-sync rastrigin 20 32 10
 run cfg5proxy_spec k_spec 0 40 "CUPSO_SYNC_MODE=spec" cuda-sync sphere 24 8 20
 run cfg5proxy_wave k_wave 5 1 "CUPSO_SYNC_MODE=wave" cuda-sync sphere 24 8 10

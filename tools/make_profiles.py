@@ -28,6 +28,8 @@ CAPTURES = {
     "cfg3_async": ("cfg3", "cuda-async", 100, 1.0, "k_async_reg<cubic,1> (registers, K=32), 2^24 x d=1, one launch = 100 iterations"),
     "cfg4_spec": ("cfg4", "cuda-sync", 60, 1.0,
                   "k_spec_split<rastrigin,8x4> (4 lanes x 8 axes per particle), 2^20 x d=32, every pass of a 60-iteration run summed"),
+    "cfg4_f32": ("cfg4", "cuda-sync-f32", 60, 1.0,
+                 "k_spec32_split<rastrigin,8x4> (FP32 engine), 2^20 x d=32, every pass of a 60-iteration run summed"),
     "cfg4_wave": ("cfg4", "cuda-sync-wave", 1, 1.0, "k_wave<rastrigin> (cos_pso), 2^20 x d=32, one iteration (iteration 5)"),
     "cfg5proxy_spec": ("cfg5", "cuda-sync", 20, 16.0,
                        "k_spec<sphere,8>, 2^24 x d=8 proxy of 2^28 (x16), every pass of a 20-iteration run summed"),
