@@ -22,6 +22,8 @@ cpu_baseline: the unmodified reference (oracle/_ref, queue-lock engine, all
 Multi-GPU (torchrun): weak scaling, each rank holds a contiguous shard of one
 swarm of world*N particles; the per-iteration gbest exchange is an NCCL
 all-gather of one (16+8d)-byte record per rank issued by libcupso on its stream.
+Engines without a sharded form (cuda-async -- SURVEY 8(e): replicas only --,
+cuda-sync-f32, the classic engines) run one independent swarm per rank instead.
 """
 from __future__ import annotations
 
@@ -261,6 +263,7 @@ def main():
     import torch
     import paper_2205_01313_b200 as cp
 
+    local = local % max(1, torch.cuda.device_count())  # more ranks than GPUs: replicas share devices
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     fitness, n_per_rank, d, T, default_variant, desc = WORKLOADS[args.workload]
@@ -282,15 +285,26 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://", world_size=world, rank=rank)
         pg = dist
-    first, count = cp.shard_range(n_total, world, rank)
+    # cuda-sync shards one swarm across the ranks (NCCL pass-record exchange);
+    # the other engines have no sharded form (cuda-async: SURVEY 8(e) "replicas
+    # only"), so at N > 1 every rank runs an independent swarm of n_per_rank
+    # particles with its own seed and no data-path collective.
+    replicas = world > 1 and variant_name != "cuda-sync"
+    if replicas:
+        p = cp.make_params(f, n_per_rank, d, T)
+        seed = 1 + rank
+        first, count = 0, n_per_rank
+    else:
+        first, count = cp.shard_range(n_total, world, rank)
 
     def barrier():
         if pg:
             pg.barrier()
         torch.cuda.synchronize()
 
-    sw = cp.Swarm(p, f, seed, device=local, first=first, count=count)
-    if world > 1:
+    sw = cp.Swarm(p, f, seed, device=local, first=first, count=count) if not replicas else \
+        cp.Swarm(p, f, seed, device=local)
+    if world > 1 and not replicas:
         uid = [cp.nccl_unique_id() if rank == 0 else None]
         pg.broadcast_object_list(uid, src=0)
         sw.nccl_init(uid[0], world, rank)
@@ -455,7 +469,8 @@ def main():
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e = {"value": n_total * T * args.steps / float(t.item()), "unit": "particle-updates/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": T * (8 + 4 + 8 + 8) + 16 + 8 * d,
-               "path": "Swarm shard API per rank: init (with NCCL adopt) + step + trace + gbest; max over ranks"}
+               "path": ("Swarm API per rank (independent replicas)" if replicas else
+                        "Swarm shard API per rank: init (with NCCL adopt)") + " + step + trace + gbest; max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -474,7 +489,8 @@ def main():
             "data": "synthetic (Philox-initialised swarm, reference make_params defaults)",
             "config": {"workload": desc, "fitness": fitness, "particles_total": n_total,
                        "particles_per_gpu": count, "dims": d, "iterations_per_step": T,
-                       "variant": variant_name, "parallelism": f"dp{world} (particle shards)",
+                       "variant": variant_name, "parallelism": f"replicas{world} (independent swarms, seeds 1..{world})" if replicas
+                       else f"dp{world} (particle shards)",
                        "sync_grid_blocks": grid,
                        "l2": "flushed (512 MiB write) before every step; within a step the swarm stays resident as in a real run"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
