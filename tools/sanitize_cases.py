@@ -15,6 +15,9 @@ CASES = [  # (fitness, n, d, T, variant, env)
     ("cubic", 5000, 1, 20, cp.SYNC, {"CUPSO_SYNC_MODE": "resident"}),
     ("cubic", 5000, 2, 10, cp.QUEUE_LOCK, {}),
     ("cubic", 5000, 2, 10, cp.REDUCTION, {}),
+    ("rosenbrock", 2001, 17, 20, cp.SYNC_F32, {}),   # k_spec32_split, ragged
+    ("rastrigin", 1001, 32, 20, cp.SYNC_F32, {}),    # k_spec32_split 8 x 4
+    ("griewank", 999, 300, 5, cp.SYNC_F32, {}),      # k_wave32 (d > 256)
 ]
 which = sys.argv[1:] and [int(x) for x in sys.argv[1].split(",")] or range(len(CASES))
 for k in which:
