@@ -427,12 +427,15 @@ __device__ __forceinline__ uint32_t warp_tmin(const uint32_t* tmin) {
 // doubles.
 // RAGGED: the swarm's d is below DL * G (any d up to 256): lane s holds the
 // valid axes of [s*DL, s*DL + DL) and skips the rest (warp-uniform tests).
-template <int F, int DL, int G, int MINB, bool SM = false, bool RAGGED = false>
+// PBSM: only the pbest columns live in shared memory (DL * blockDim doubles):
+// read once per axis-iteration (one LDS), written on the rare improvement.
+template <int F, int DL, int G, int MINB, bool SM = false, bool RAGGED = false, bool PBSM = false>
 __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KState S0, KState S1, KCtl C,
                                                                   SpecCtl* sc, uint32_t t_end, uint32_t kmax,
                                                                   unsigned char* rec_out, int sharded) {
   constexpr int D = DL * G;
   static_assert(!(SM && RAGGED), "the SMEM-state split kernel needs d == DL * G");
+  static_assert(!(SM && PBSM), "PBSM keeps only the pbest columns in SMEM");
   extern __shared__ double s_state[];
   static_assert(32 % G == 0, "G must divide the warp");
   __shared__ double s_gpos[D];
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
     const uint32_t li = u0 + lane / G;
     const bool live = li < P.n;
     const uint32_t gi = P.base + li;
-    double rx[SM ? 1 : DL], rv[SM ? 1 : DL], rpb[SM ? 1 : DL], pbf = -INFINITY;
+    double rx[SM ? 1 : DL], rv[SM ? 1 : DL], rpb[SM || PBSM ? 1 : DL], pbf = -INFINITY;
     const uint32_t bd = blockDim.x;
     auto X = [&](int a) -> double& {
       if constexpr (SM) return s_state[(0 * DL + a) * bd + tid]; else return rx[a];
@@ -486,7 +489,9 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
       if constexpr (SM) return s_state[(1 * DL + a) * bd + tid]; else return rv[a];
     };
     auto PB = [&](int a) -> double& {
-      if constexpr (SM) return s_state[(2 * DL + a) * bd + tid]; else return rpb[a];
+      if constexpr (SM) return s_state[(2 * DL + a) * bd + tid];
+      else if constexpr (PBSM) return s_state[a * bd + tid];
+      else return rpb[a];
     };
     if (live) {
 #pragma unroll
