@@ -143,7 +143,7 @@ def test_spec_single_particle_and_single_iteration(cupso, oracle, spec_env):
         compare_state(got["state"], orc, "sphere", f"n={n} T={T}")
 
 
-@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7", "8"])
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10"])
 def test_spec_split_tunings_agree(cupso, oracle, monkeypatch, cfg):
     """d = 32 (the cfg4 shape): every lanes-per-particle split of k_spec_split is bit-identical."""
     monkeypatch.setenv("CUPSO_SYNC_MODE", "spec")
@@ -158,6 +158,21 @@ def test_spec_split_tunings_agree(cupso, oracle, monkeypatch, cfg):
     orc_c = oracle.run_serial("cubic", n, d, T, seed)
     assert_bitwise(got_c["trace"], orc_c.trace, "cubic trace")
     compare_state(got_c["state"], orc_c, "cubic", f"cfg {cfg}")
+
+
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("fit", ["rastrigin", "sphere"])
+def test_spec_d8_tunings_agree(cupso, oracle, monkeypatch, cfg, fit):
+    """d = 8: k_spec at 1-3 blocks/SM and the one-lane split kernel with the
+    pbest column in SMEM (the rastrigin default) are bit-identical."""
+    monkeypatch.setenv("CUPSO_SYNC_MODE", "spec")
+    monkeypatch.setenv("CUPSO_SPEC_CFG", cfg)
+    n, d, T, seed = 3001, 8, 80, 6
+    got = run_sync(cupso, fit, n, d, T, seed)
+    assert got["mode"] == "spec"
+    orc = oracle.run_serial(fit, n, d, T, seed)
+    assert np.array_equal(got["trace_particle"], orc.trace_particle)
+    compare_state(got["state"], orc, fit, f"cfg {cfg}")
 
 
 def test_spec_cfg5_shape_equals_wave(cupso, monkeypatch):
