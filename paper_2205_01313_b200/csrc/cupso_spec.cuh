@@ -427,9 +427,10 @@ __device__ __forceinline__ uint32_t warp_tmin(const uint32_t* tmin) {
 // doubles.
 // RAGGED: the swarm's d is below DL * G (any d up to 256): lane s holds the
 // valid axes of [s*DL, s*DL + DL) and skips the rest (warp-uniform tests).
-// PBSM: only the pbest columns live in shared memory (DL * blockDim doubles):
-// read once per axis-iteration (one LDS), written on the rare improvement.
-template <int F, int DL, int G, int MINB, bool SM = false, bool RAGGED = false, bool PBSM = false>
+// PBSM = 1: only the pbest columns live in shared memory (DL * blockDim
+// doubles): read once per axis-iteration (one LDS), written on the rare
+// improvement. PBSM = 2: the velocity columns too (one LDS + one STS more).
+template <int F, int DL, int G, int MINB, bool SM = false, bool RAGGED = false, int PBSM = 0>
 __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KState S0, KState S1, KCtl C,
                                                                   SpecCtl* sc, uint32_t t_end, uint32_t kmax,
                                                                   unsigned char* rec_out, int sharded) {
@@ -480,13 +481,15 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
     const uint32_t li = u0 + lane / G;
     const bool live = li < P.n;
     const uint32_t gi = P.base + li;
-    double rx[SM ? 1 : DL], rv[SM ? 1 : DL], rpb[SM || PBSM ? 1 : DL], pbf = -INFINITY;
+    double rx[SM ? 1 : DL], rv[SM || PBSM >= 2 ? 1 : DL], rpb[SM || PBSM ? 1 : DL], pbf = -INFINITY;
     const uint32_t bd = blockDim.x;
     auto X = [&](int a) -> double& {
       if constexpr (SM) return s_state[(0 * DL + a) * bd + tid]; else return rx[a];
     };
     auto V = [&](int a) -> double& {
-      if constexpr (SM) return s_state[(1 * DL + a) * bd + tid]; else return rv[a];
+      if constexpr (SM) return s_state[(1 * DL + a) * bd + tid];
+      else if constexpr (PBSM >= 2) return s_state[(DL + a) * bd + tid];
+      else return rv[a];
     };
     auto PB = [&](int a) -> double& {
       if constexpr (SM) return s_state[(2 * DL + a) * bd + tid];
