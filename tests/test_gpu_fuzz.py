@@ -1,0 +1,57 @@
+"""GPU: randomised parity soak of the synchronous engines against the oracle.
+
+Each trial draws a fitness with an exact (cos-free) fitness, a particle count,
+a dimension (1..256, so every kernel family is hit: k_spec, the split kernels
+ragged or not, the wave / persistent fallbacks past 256 are covered
+elsewhere), a 64-bit seed, a pass-length cap (CUPSO_SPEC_K) and a random
+chunking of the iterations with a random deterministic engine per chunk
+(cuda-sync, reduction, unrolled, queue, queue-lock). The trace, the gbest index
+trajectory and the final state must equal run_serial bit for bit
+(engine_serial.hpp:13-44). FUZZ_TRIALS (default 12) and FUZZ_SEED size a run.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+TRIALS = int(os.environ.get("FUZZ_TRIALS", "12"))
+BASE = int(os.environ.get("FUZZ_SEED", "20261017"))
+
+
+def draw_case(rng):
+    fit = rng.choice(["cubic", "sphere", "rosenbrock"])
+    d = int(rng.choice([1, 1, 2, 3, 4, 5, 7, 8, 8, 9, 12, 16, 17, 31, 32, 33, 64, 100, 129, 256]))
+    n = int(rng.integers(1, max(2, 200_000 // (d * 40))))
+    T = int(rng.integers(1, 90))
+    seed = int(rng.integers(0, 2**64 - 1, dtype=np.uint64))
+    kmax = str(rng.choice([1, 2, 3, 5, 16, 64]))
+    cuts = sorted(set(int(x) for x in rng.integers(1, T, size=int(rng.integers(0, 4))))) if T > 1 else []
+    bounds = [0] + cuts + [T]
+    chunks = [b - a for a, b in zip(bounds, bounds[1:]) if b > a]
+    engines = [str(rng.choice(["cuda-sync", "cuda-sync", "cuda-reduction", "cuda-unrolled", "cuda-queue",
+                               "cuda-queue-lock"])) for _ in chunks]
+    return fit, n, d, T, seed, kmax, chunks, engines
+
+
+@pytest.mark.parametrize("trial", range(TRIALS))
+def test_fuzz_sync_engines_match_serial(cupso, oracle, monkeypatch, trial):
+    rng = np.random.default_rng(BASE + trial)
+    fit, n, d, T, seed, kmax, chunks, engines = draw_case(rng)
+    what = f"{fit} n={n} d={d} T={T} seed={seed} K<={kmax} chunks={chunks} engines={engines}"
+    monkeypatch.setenv("CUPSO_SPEC_K", kmax)
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, seed) as sw:
+        for c, e in zip(chunks, engines):
+            sw.step(cupso.find_engine(e).variant, c)
+        tr, tp, _ = sw.trace()
+        st = sw.state()
+    orc = oracle.run_serial(fit, n, d, T, seed)
+    assert_bitwise(tr, orc.trace, f"{what}: trace")
+    assert np.array_equal(tp, orc.trace_particle), f"{what}: gbest index trajectory"
+    for k in ("positions", "velocities", "pbest_pos", "pbest_fit", "fitness"):
+        assert_bitwise(getattr(st, k), orc.state[k], f"{what}: {k}")
