@@ -55,3 +55,67 @@ def test_fuzz_sync_engines_match_serial(cupso, oracle, monkeypatch, trial):
     assert np.array_equal(tp, orc.trace_particle), f"{what}: gbest index trajectory"
     for k in ("positions", "velocities", "pbest_pos", "pbest_fit", "fitness"):
         assert_bitwise(getattr(st, k), orc.state[k], f"{what}: {k}")
+
+
+SHARD_TRIALS = int(os.environ.get("FUZZ_SHARD_TRIALS", "4"))
+
+
+@pytest.mark.parametrize("trial", range(SHARD_TRIALS))
+def test_fuzz_shards_match_single_swarm(cupso, monkeypatch, trial):
+    """Random shard counts (2-4) of random swarms, host-thread all-gather or the
+    in-kernel peer-memory exchange, random chunking: every shard's trace and
+    gbest index trajectory equal the single swarm's, and the concatenated shard
+    positions equal its state, bit for bit."""
+    import threading
+
+    from test_gpu_scale import _ThreadAllGather, same
+    rng = np.random.default_rng(BASE + 10_000 + trial)
+    fit = str(rng.choice(["cubic", "sphere", "rosenbrock"]))
+    d = int(rng.choice([1, 2, 4, 5, 8, 12, 32, 64]))
+    shards = int(rng.integers(2, 5))
+    n = int(rng.integers(shards, max(shards + 1, 120_000 // (d * 20))))
+    T = int(rng.integers(2, 70))
+    seed = int(rng.integers(0, 2**63))
+    p2p = bool(rng.integers(0, 2))
+    monkeypatch.setenv("CUPSO_SPEC_K", str(rng.choice([2, 8, 64])))
+    cut = int(rng.integers(1, T))
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, seed) as whole:
+        whole.step(cupso.SYNC, T)
+        wtr, wtp, _ = whole.trace()
+        wst = whole.state()
+    parts = [cupso.Swarm(p, f, seed, first=a, count=c, init=False)
+             for a, c in (cupso.shard_range(n, shards, r) for r in range(shards))]
+    what = f"{fit} n={n} d={d} T={T} shards={shards} p2p={p2p} cut={cut}"
+    try:
+        cupso.init_shards(parts)
+        if p2p:
+            cupso.p2p_shards(parts)
+        ag = _ThreadAllGather(shards)
+        errs = []
+
+        def run(r):
+            try:
+                for c in (cut, T - cut):
+                    if p2p:
+                        parts[r].step(cupso.SYNC, c)
+                    else:
+                        parts[r].step_exchange(c, shards, lambda loc: ag(r, loc))
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(shards)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        assert not errs, (what, errs)
+        for sh in parts:
+            tr, tp, _ = sh.trace()
+            assert same(tr, wtr) and np.array_equal(tp, wtp), what
+        pos = np.concatenate([sh.state().positions.reshape(d, -1) for sh in parts], axis=1)
+        assert same(pos.reshape(-1), wst.positions), what
+    finally:
+        for sh in parts:
+            sh.close()
