@@ -119,3 +119,46 @@ def test_fuzz_shards_match_single_swarm(cupso, monkeypatch, trial):
     finally:
         for sh in parts:
             sh.close()
+
+
+STAT_TRIALS = int(os.environ.get("FUZZ_STAT_TRIALS", "6"))
+
+
+@pytest.mark.parametrize("trial", range(STAT_TRIALS))
+def test_fuzz_statistical_engines_invariants(cupso, oracle, monkeypatch, trial):
+    """cuda-async (every schedule) and cuda-sync-f32 on random shapes, any
+    fitness: a monotone trace ending at the gbest; the gbest record is a
+    consistent (fitness, position) pair that equals the best pbest (at FP32 for
+    the FP32 engine); the state stays in the box."""
+    rng = np.random.default_rng(BASE + 20_000 + trial)
+    fit = str(rng.choice(["cubic", "sphere", "rosenbrock", "griewank", "rastrigin"]))
+    d = int(rng.choice([1, 2, 3, 4, 8, 9, 16, 32, 33, 100, 256]))
+    n = int(rng.integers(1, max(2, 150_000 // (d * 20))))
+    T = int(rng.integers(2, 60))
+    seed = int(rng.integers(0, 2**63))
+    engine = str(rng.choice(["cuda-async", "cuda-sync-f32"]))
+    if engine == "cuda-async":
+        monkeypatch.setenv("CUPSO_ASYNC_MODE", str(rng.choice(["reg", "tiled", "plain"])))
+        monkeypatch.setenv("CUPSO_ASYNC_K", str(rng.choice([1, 5, 32])))
+    what = f"{engine} {fit} n={n} d={d} T={T} seed={seed}"
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    cut = int(rng.integers(1, T))
+    with cupso.Swarm(p, f, seed) as sw:
+        init_fit = sw.initial_gbest()[0]
+        for c in (cut, T - cut):
+            sw.step(cupso.find_engine(engine).variant, c)
+        tr, tp, occ = sw.trace()
+        gb = sw.gbest()
+        st = sw.state()
+    assert (np.diff(tr) >= 0).all() and tr[0] >= init_fit, what
+    assert tr[-1] == gb.fit and 0 <= gb.particle < n, what
+    assert ((occ >= 0) & (occ <= 1)).all(), what
+    rel = 1e-4 if engine == "cuda-sync-f32" else 1e-9
+    assert abs(oracle.fitness(fit, gb.pos) - gb.fit) <= rel * max(1.0, abs(gb.fit)), what
+    if engine == "cuda-sync-f32":
+        assert np.float32(gb.fit) == np.float32(st.pbest_fit.max()), what
+        assert (np.abs(st.positions) <= np.float32(f.hi)).all(), what
+    else:
+        assert gb.fit == st.pbest_fit.max(), what
+        assert (np.abs(st.positions) <= f.hi).all(), what
