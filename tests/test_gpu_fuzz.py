@@ -162,3 +162,31 @@ def test_fuzz_statistical_engines_invariants(cupso, oracle, monkeypatch, trial):
     else:
         assert gb.fit == st.pbest_fit.max(), what
         assert (np.abs(st.positions) <= f.hi).all(), what
+
+
+COS_TRIALS = int(os.environ.get("FUZZ_COS_TRIALS", "3"))
+
+
+@pytest.mark.parametrize("trial", range(COS_TRIALS))
+def test_fuzz_cos_fitness_sync_close_to_serial(cupso, oracle, monkeypatch, trial):
+    """griewank / rastrigin through cuda-sync: the device cos is within 2 ulp of
+    glibc's, not bitwise (section 2), so the trace and the state are compared at
+    the cos tolerance -- a gbest race decided by that last ulp would show up here."""
+    from test_gpu_parity import assert_close
+    rng = np.random.default_rng(BASE + 30_000 + trial)
+    fit = str(rng.choice(["griewank", "rastrigin"]))
+    d = int(rng.choice([1, 2, 3, 4, 8, 12, 16, 32, 64]))
+    n = int(rng.integers(1, max(2, 60_000 // (d * 20))))
+    T = int(rng.integers(1, 60))
+    seed = int(rng.integers(0, 2**63))
+    what = f"{fit} n={n} d={d} T={T} seed={seed}"
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, seed) as sw:
+        sw.step(cupso.SYNC, T)
+        tr, tp, _ = sw.trace()
+        st = sw.state()
+    orc = oracle.run_serial(fit, n, d, T, seed)
+    assert np.array_equal(tp, orc.trace_particle), f"{what}: gbest index trajectory"
+    assert_close(tr, orc.trace, f"{what}: trace")
+    assert_close(st.positions, orc.state["positions"], f"{what}: positions")
