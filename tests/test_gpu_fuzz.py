@@ -7,7 +7,7 @@ elsewhere), a 64-bit seed, a pass-length cap (CUPSO_SPEC_K) and a random
 chunking of the iterations with a random deterministic engine per chunk
 (cuda-sync, reduction, unrolled, queue, queue-lock). The trace, the gbest index
 trajectory and the final state must equal run_serial bit for bit
-(engine_serial.hpp:13-44). FUZZ_TRIALS (default 12) and FUZZ_SEED size a run.
+(engine_serial.hpp:13-44). FUZZ_TRIALS (default 12), FUZZ_SEED and FUZZ_CELLS size a run.
 """
 import os
 
@@ -20,12 +20,13 @@ pytestmark = pytest.mark.gpu
 
 TRIALS = int(os.environ.get("FUZZ_TRIALS", "12"))
 BASE = int(os.environ.get("FUZZ_SEED", "20261017"))
+CELLS = int(os.environ.get("FUZZ_CELLS", "200000"))  # bounds n * d * 40 of the exact-fitness trials
 
 
 def draw_case(rng):
     fit = rng.choice(["cubic", "sphere", "rosenbrock"])
     d = int(rng.choice([1, 1, 2, 3, 4, 5, 7, 8, 8, 9, 12, 16, 17, 31, 32, 33, 64, 100, 129, 256]))
-    n = int(rng.integers(1, max(2, 200_000 // (d * 40))))
+    n = int(rng.integers(1, max(2, CELLS // (d * 40))))
     T = int(rng.integers(1, 90))
     seed = int(rng.integers(0, 2**64 - 1, dtype=np.uint64))
     kmax = str(rng.choice([1, 2, 3, 5, 16, 64]))
