@@ -8,22 +8,33 @@ One bench "step" = one full optimisation run of the workload's T iterations
 (init_swarm excluded, exactly like the reference's compute_seconds,
 engine_serial.hpp:25-40), with the swarm resident in HBM. The default
 workload is BASELINE.json configs[1]: 1-D cubic, 2^20 particles, 1000
-iterations, synchronous atomic variant (cuda-sync); the in-repo reduction
-baseline kernel (cuda-reduction) is timed on the same workload in the same run.
+iterations, synchronous variant (cuda-sync).
 
-value   = particles * iterations * steps * world / max-over-ranks device seconds
+value   = particles * iterations * steps / max-over-ranks device seconds
 e2e     = the same metric through the reference-facing C-ABI call cupso_run
-          (host params in, host trace/gbest out, allocation + init + H2D/D2H
-          inside the timed region), wall clock
-roofline: algorithmic bytes (5d+1)*8 per particle-update per
-          launch / CUDA-event duration of that launch, against MEASURED_PEAKS.json
+          (host params in, host trace/gbest out, init + H2D/D2H inside the
+          timed region), wall clock
+roofline: the binding roof of the dominant kernel. The temporally blocked
+          kernels (k_spec, k_async_reg) keep the swarm in registers for a whole
+          pass, so HBM does not bind them: their roof is instruction issue --
+          warp-instructions of the exact timed schedule (ncu capture committed in
+          profiles/ncu_bench_r02.json) / device time / (SMs x 4 x SM clock). The
+          HBM model of SURVEY 8(d) ((5d+1)*8 algorithmic bytes per
+          particle-update / launch time / MEASURED_PEAKS hbm_gbs) stays as
+          roofline.hbm_model; `traffic` is the captured DRAM bytes per launch.
+paper_engines: the paper's per-iteration engines (reduction, unrolled, queue,
+          queue-lock) and cuda-sync without temporal blocking (wave mode) on the
+          same workload, so the gain splits into aggregation and blocking.
+strong_cfg5: BASELINE configs[4] as a strong-scaling sub-record on every line:
+          sphere d=8, 2^28 particles in total, 2^28/N per GPU.
 cpu_baseline: the unmodified reference (oracle/_ref, queue-lock engine, all
-          host threads) on a bounded sample of the same workload, rank 0 only
-Multi-GPU (torchrun): weak scaling, each rank holds a contiguous shard of one
-swarm of world*N particles; the per-iteration gbest exchange is an NCCL
-all-gather of one (16+8d)-byte record per rank issued by libcupso on its stream.
-Engines without a sharded form (cuda-async -- SURVEY 8(e): replicas only --,
-cuda-sync-f32, the classic engines) run one independent swarm per rank instead.
+          host threads) on a bounded sample of the same workload, rank 0 only.
+Multi-GPU: `--gpus N` without WORLD_SIZE re-launches itself under
+torch.distributed.run (N ranks, one per GPU); under torchrun it checks
+WORLD_SIZE == N. cuda-sync shards one swarm across the ranks (contiguous
+global-index ranges; one NCCL all-gather of a pass record per pass);
+engines without a sharded form (cuda-async -- SURVEY 8(e): replicas only --,
+cuda-sync-f32, the classic engines) run one independent swarm per rank.
 """
 from __future__ import annotations
 
@@ -31,6 +42,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,9 +57,13 @@ WORKLOADS = {
     "cfg2": ("cubic", 1 << 20, 1, 1000, "cuda-sync", "BASELINE configs[1]: 1-D cubic, 2^20 particles, 1000 iterations"),
     "cfg3": ("cubic", 1 << 24, 1, 100, "cuda-async", "BASELINE configs[2]: 1-D cubic, 2^24 particles, async persistent"),
     "cfg4": ("rastrigin", 1 << 20, 32, 1000, "cuda-sync", "BASELINE configs[3]: Rastrigin d=32, 2^20 particles, 1000 iterations"),
-    "cfg5": ("sphere", 1 << 28, 8, 50, "cuda-sync", "BASELINE configs[4]: sphere d=8, 2^28 particles (per GPU: 2^28/N)"),
+    "cfg5": ("sphere", 1 << 28, 8, 200, "cuda-sync", "BASELINE configs[4]: sphere d=8, 2^28 particles (per GPU: 2^28/N), 200 iterations"),
 }
+STRONG = ("sphere", 1 << 28, 8, 200)  # the strong_cfg5 sub-record
+STRONG_MAX_STEPS = 5
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+PAPER_ENGINES = ("cuda-reduction", "cuda-unrolled", "cuda-queue", "cuda-queue-lock")
+NCU_BENCH = os.path.join(ROOT, "profiles", "ncu_bench_r02.json")
 
 
 def dist_env():
@@ -55,6 +71,20 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args_list, n) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run and pass rank 0's JSON line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + args_list
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -127,64 +157,16 @@ def measured_peak_gbs():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_entry(workload: str, variant: str) -> dict:
-    """The committed ncu summary entry (profiles/ncu_summary_*.json) for a kernel, or {}."""
-    pdir = os.path.join(ROOT, "profiles")
-    for name in sorted(os.listdir(pdir), reverse=True) if os.path.isdir(pdir) else []:
-        if name.startswith("ncu_summary") and name.endswith(".json"):
-            try:
-                with open(os.path.join(pdir, name)) as fh:
-                    e = json.load(fh).get(workload, {}).get(variant)
-                if e and e.get("dram_bytes_per_launch") is not None:
-                    return e
-            except Exception:
-                pass
-    return {}
+def ncu_bench_entry(workload: str, variant: str) -> dict:
+    """The committed ncu capture of the exact timed schedule (tools/ncu_bench.py), or {}."""
+    try:
+        with open(NCU_BENCH) as fh:
+            return json.load(fh).get(workload, {}).get(variant, {})
+    except Exception:
+        return {}
 
 
-def ncu_traffic(workload: str, variant: str):
-    """(dram bytes per iteration, 1) from the committed ncu summary, or (None, None)."""
-    e = ncu_entry(workload, variant)
-    if not e:
-        return None, None
-    if e.get("dram_bytes_per_iter") is not None:
-        return e["dram_bytes_per_iter"], 1
-    return e["dram_bytes_per_launch"], e.get("iters_per_launch")
-
-
-def cpu_reference_leg(fitness, n, d, max_seconds=12.0, sample_iters=None):
-    """The unmodified reference (oracle/_ref) queue-lock engine on all host threads,
-    timed on a bounded sample of the workload. Checker/baseline only."""
-    import oracle as orc
-    if not os.path.exists(orc.REF_SO):
-        if os.path.isdir(orc.REF_INC):
-            orc.build(ref=True)
-    if os.path.exists(orc.REF_SO):
-        kind = "reference"
-        ref = orc.Reference()
-        threads = os.cpu_count() or 1
-        # calibrate: 2 iterations, then size the sample to ~max_seconds
-        r, _ = ref.run("queue-lock", fitness, n, d, 2, 1, threads=threads, want_particles=False)
-        per_iter = max(r.compute_seconds / 2, 1e-6)
-        iters = sample_iters or max(2, min(1000, int(max_seconds / per_iter)))
-        r, _ = ref.run("queue-lock", fitness, n, d, iters, 1, threads=threads, want_particles=False)
-        secs = r.compute_seconds
-        engine = "queue-lock"
-    else:  # the C restatement, single thread
-        kind = "port"
-        o = orc.Oracle()
-        threads = 1
-        r = o.run_serial(fitness, n, d, 2, 1, want_state=False)
-        per_iter = max(r.compute_seconds / 2, 1e-6)
-        iters = sample_iters or max(2, min(1000, int(max_seconds / per_iter)))
-        r = o.run_serial(fitness, n, d, iters, 1, want_state=False)
-        secs = r.compute_seconds
-        engine = "serial (oracle/pso_oracle.c)"
-    return {"value": n * iters / secs, "unit": "particle-updates/s", "cores": threads, "kind": kind,
-            "sample": f"{engine}: {fitness} d={d}, {n} particles x {iters} iterations "
-                      f"(compute loop {secs:.2f} s, seed 1, cpu={_cpu_model()})"}
-
-
+# ------------------------------------------------------------ CPU reference
 def _cpu_model():
     try:
         with open("/proc/cpuinfo") as fh:
@@ -196,52 +178,302 @@ def _cpu_model():
     return "unknown"
 
 
-def run_reference_arm(args, world, rank):
-    if rank != 0:
-        return 0
-    fitness, n, d, T, _, desc = WORKLOADS[args.workload]
-    n_rank = n if args.workload != "cfg5" else (1 << 24)  # 2^28 FP64 state does not fit host RAM budget
+def _reference_runner():
+    """(kind, threads, run(fitness, n, d, iters) -> compute seconds, engine name).
+    The unmodified reference (oracle/_ref, queue-lock, all host threads) where it
+    was built, else the C restatement's serial loop. Checker/baseline only."""
     import oracle as orc
     if not os.path.exists(orc.REF_SO) and os.path.isdir(orc.REF_INC):
         orc.build(ref=True)
-    base = cpu_reference_leg(fitness, n_rank, d, max_seconds=3.0)
-    # each step: a bounded sample run of the same workload
-    iters = int(base["sample"].split(" x ")[1].split(" ")[0])
-    vals = []
-    if base["kind"] == "reference":
+    if os.path.exists(orc.REF_SO):
         ref = orc.Reference()
-        for k in range(args.warmup + args.steps):
-            r, _ = ref.run("queue-lock", fitness, n_rank, d, iters, 1, threads=base["cores"], want_particles=False)
-            if k >= args.warmup:
-                vals.append(r.compute_seconds)
-    else:
-        o = orc.Oracle()
-        for k in range(args.warmup + args.steps):
-            r = o.run_serial(fitness, n_rank, d, iters, 1, want_state=False)
-            if k >= args.warmup:
-                vals.append(r.compute_seconds)
+        threads = os.cpu_count() or 1
+
+        def run(fitness, n, d, iters):
+            r, _ = ref.run("queue-lock", fitness, n, d, iters, 1, threads=threads, want_particles=False)
+            return r.compute_seconds
+        return "reference", threads, run, "queue-lock (oracle/_ref, the unmodified reference)"
+    o = orc.Oracle()
+
+    def run(fitness, n, d, iters):
+        return o.run_serial(fitness, n, d, iters, 1, want_state=False).compute_seconds
+    return "port", 1, run, "serial (oracle/pso_oracle.c)"
+
+
+def cpu_reference_leg(fitness, n, d, T, max_seconds=12.0):
+    """The reference on a bounded sample of the workload (~max_seconds)."""
+    kind, threads, run, engine = _reference_runner()
+    per_iter = max(run(fitness, n, d, 2) / 2, 1e-6)
+    iters = max(2, min(T, int(max_seconds / per_iter)))
+    secs = run(fitness, n, d, iters)
+    return {"value": n * iters / secs, "unit": "particle-updates/s", "cores": threads, "kind": kind,
+            "sample": f"{engine}: {fitness} d={d}, {n} particles x {iters} of {T} iterations "
+                      f"(compute loop {secs:.2f} s, seed 1, cpu={_cpu_model()})"}
+
+
+def run_reference_arm(args, world, rank):
+    """The reference's own CPU implementation on the same workload: the full T
+    iterations per step when a step fits STEP_BUDGET seconds (cfg2: ~8 s on 16
+    host cores), else a bounded sample of the iterations (a rate: the
+    per-iteration cost is flat)."""
+    if rank != 0:
+        return 0
+    step_budget = 15.0
+    fitness, n, d, T, _, desc = WORKLOADS[args.workload]
+    if args.iters:
+        T = args.iters
+    n_rank = n if args.workload != "cfg5" else (1 << 24)  # 2^28 FP64 state would need ~56 GB of host RAM
+    kind, threads, run, engine = _reference_runner()
+    per_iter = max(run(fitness, n_rank, d, 2) / 2, 1e-6)
+    iters = T if per_iter * T <= step_budget else max(2, int(step_budget / per_iter))
+    vals = []
+    for k in range(args.warmup + args.steps):
+        s = run(fitness, n_rank, d, iters)
+        if k >= args.warmup:
+            vals.append(s)
     secs = sum(vals)
     value = n_rank * iters * len(vals) / secs
+    same = iters == T and n_rank == n
     line = {
         "impl": "reference", "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * secs / len(vals), "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak",
+        "ms_per_step": 1e3 * secs / len(vals), "higher_is_better": True,
+        "scaling": "strong" if args.workload == "cfg5" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox init of the reference)",
         "config": {"workload": desc, "fitness": fitness, "particles": n_rank, "dims": d,
-                   "iterations_per_step": iters, "engine": "reference queue-lock (all host threads)"},
-        "cpu_baseline": {**base, "value": value},
+                   "iterations_per_step": iters, "iterations_of_workload": T, "same_config": same,
+                   "engine": f"reference {engine}, {threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": "particle-updates/s", "cores": threads, "kind": kind,
+                         "sample": f"{fitness} d={d}, {n_rank} particles x {iters} iterations per step, "
+                                   f"cpu={_cpu_model()}"},
         "e2e": {"value": value, "unit": "particle-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------ GPU arm
 def flush_l2(torch, dev):
     buf = getattr(flush_l2, "buf", None)
     if buf is None:
         buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
         flush_l2.buf = buf
     buf.random_(0, 1 << 30)
+
+
+class Job:
+    """One swarm (or shard / replica) per rank and the timing protocol: W untimed
+    warm-up steps, then K steps, each = init_swarm + L2 flush (untimed) + the T
+    iterations timed with CUDA events on the launching stream; barrier + sync on
+    both sides; max over ranks of the summed device seconds."""
+
+    def __init__(self, cp, torch, pg, dev, local, world, rank, fitness, n_total, d, T, variant, sharded_total):
+        self.cp, self.torch, self.pg, self.dev, self.local = cp, torch, pg, dev, local
+        self.world, self.rank = world, rank
+        self.engine = cp.find_engine(variant)
+        self.variant = variant
+        self.f = cp.find_fitness(fitness)
+        self.T, self.d = T, d
+        # cuda-sync shards one swarm; the other engines run one swarm per rank
+        self.replicas = world > 1 and variant != "cuda-sync"
+        if self.replicas:
+            n_rank = n_total // world if sharded_total else n_total
+            self.p = cp.make_params(self.f, n_rank, d, T)
+            self.seed, first, self.count = 1 + rank, 0, n_rank
+            self.n_total = n_rank * world
+            self.sw = cp.Swarm(self.p, self.f, self.seed, device=local)
+        else:
+            self.n_total = n_total if sharded_total else n_total * world
+            self.p = cp.make_params(self.f, self.n_total, d, T)
+            self.seed = 1
+            first, self.count = cp.shard_range(self.n_total, world, rank)
+            self.sw = cp.Swarm(self.p, self.f, self.seed, device=local, first=first, count=self.count)
+            if world > 1:
+                uid = [cp.nccl_unique_id() if rank == 0 else None]
+                pg.broadcast_object_list(uid, src=0)
+                self.sw.nccl_init(uid[0], world, rank)
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x: float) -> float:
+        if not self.pg:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def run(self, warmup: int, steps: int, variant=None, clocks=None):
+        v = (variant or self.engine).variant
+        for _ in range(warmup):
+            self.sw.init()
+            flush_l2(self.torch, self.dev)
+            self.barrier()
+            self.sw.step(v, self.T)
+        per = []
+        self.barrier()
+        self.spec_at_start = self.sw.spec_stats()  # pass counters of the timed steps only
+        ctx = clocks if clocks is not None else _Null()
+        with ctx:
+            for _ in range(steps):
+                self.sw.init()
+                flush_l2(self.torch, self.dev)
+                self.barrier()
+                per.append(self.sw.step(v, self.T))
+            self.barrier()
+        return self.max_over_ranks(sum(per)), len(per)
+
+    def close(self):
+        self.sw.close()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def roofline_of(job, workload, variant, dev_secs, K, clocks, spec_delta, torch):
+    """Binding roof of the dominant kernel, see the module docstring."""
+    cp, sw, T, d = job.cp, job.sw, job.T, job.d
+    f32 = variant == "cuda-sync-f32"
+    bytes_per_pu = (5 * d + 1) * (4 if f32 else 8)
+    mode = sw.sync_mode() if variant == "cuda-sync" else ("spec" if f32 else None)
+    amode = sw.async_mode() if variant == "cuda-async" else None
+    passes, fails, launches = (x / K for x in spec_delta)
+    spec = mode in ("spec", "nccl-sharded-spec")
+    grid = sw.sync_grid_blocks()
+    persistent = variant == "cuda-async" or (variant == "cuda-sync" and job.world == 1 and grid > 0 and not spec)
+    launches_per_step = {"cuda-sync": (launches * (2 if job.world > 1 else 1)) if spec else
+                         (1 if persistent else (2 * T if job.world > 1 else T)), "cuda-async": 1,
+                         "cuda-queue-lock": T, "cuda-queue": 2 * T, "cuda-reduction": 2 * T,
+                         "cuda-unrolled": 2 * T, "cuda-sync-f32": launches}[variant]
+    iters_per_launch = T if persistent else (T / passes if spec and passes else 1)
+    launch_secs = (dev_secs / K) / (T / iters_per_launch)
+    alg_bytes = job.count * iters_per_launch * bytes_per_pu
+    peak, peak_src = measured_peak_gbs()
+    achieved = alg_bytes / launch_secs / 1e9
+    fit = job.f.name
+    kernel = {"resident": f"k_sync_res<{fit},{d}>", "persistent": f"k_sync<{fit}>", "wave": f"k_wave<{fit}>",
+              "spec": f"k_spec<{fit},{d}>", "nccl-sharded-spec": f"k_spec<{fit},{d}>+k_spec_commit"}.get(
+                  mode, f"k_propose<{fit}>+k_commit")
+    if f32:
+        kernel = f"k_spec32<{fit},{d}>"
+    if variant == "cuda-async":
+        kernel = {"reg": f"k_async_reg<{fit},{d}>", "tiled": f"k_async_tiled<{fit}>"}.get(amode, f"k_async<{fit}>")
+    elif variant not in ("cuda-sync", "cuda-sync-f32"):
+        kernel = f"k_classic_step<{fit}>"
+    hbm = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
+           "bytes_per_particle_update": bytes_per_pu}
+    e = ncu_bench_entry(workload, variant) if job.world == 1 else {}
+    traffic = None
+    if e.get("dram_bytes_per_step") is not None and e.get("launches_per_step"):
+        traffic = e["dram_bytes_per_step"] / e["launches_per_step"]
+    blocked = mode in ("resident", "spec", "nccl-sharded-spec") or amode == "reg"
+    sm_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
+    nsm = torch.cuda.get_device_properties(job.dev).multi_processor_count
+    roof = None
+    if blocked and e.get("warp_inst_per_step"):
+        ach = e["warp_inst_per_step"] * K / dev_secs  # warp-instructions per second, live device time
+        peak_i = nsm * 4 * sm_hz
+        roof = {"bound": "issue", "achieved": ach / 1e9, "peak": peak_i / 1e9, "unit": "G warp-instructions/s",
+                "frac": ach / peak_i, "traffic": traffic,
+                "inst_per_particle_update": e["warp_inst_per_step"] * 32 / (job.count * T),
+                "peak_source": f"{nsm} SMs x 4 schedulers x SM clock {sm_hz / 1e6:.0f} MHz (NVML, timed region)",
+                "source": f"smsp__inst_executed.sum over the exact timed schedule ({e.get('capture', '?')})"}
+    if roof is None:  # streaming kernels: the HBM model binds
+        roof = dict(hbm, traffic=traffic)
+    roof.update({"kernel": kernel, "mode": mode or amode, "hbm_model": hbm,
+                 "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over "
+                                 "the launches of one timed step (profiles/ncu_bench_r02.json)"})
+    if blocked:
+        roof["note"] = ("temporally blocked: each pass reads and writes the state once for K iterations held "
+                        "in registers, so the HBM model (hbm_model.frac > 1) does not bind; instruction issue does")
+    # RNG ceiling: the reference's two Philox-4x32-10 calls per particle-axis alone
+    # run at 3.11e11 draw pairs/s on a B200 (profiles/micro_philox_r01.txt); the
+    # FP32 engine draws one call per particle-axis and iteration pair (4x fewer)
+    draws_ps = 3.114e11 * (4.0 if f32 else 1.0)
+    value = job.n_total * T * K / dev_secs
+    rng_peak = draws_ps / d * job.world
+    roof["rng_ceiling"] = {"bound": "issue (Philox IMAD.WIDE/LOP3)", "achieved": value, "peak": rng_peak,
+                           "unit": "particle-updates/s", "frac": value / rng_peak,
+                           "source": "profiles/micro_philox_r01.txt (draw-only microbenchmark, 1 GPU)"}
+    if spec:
+        roof["spec"] = {"passes_per_step": passes, "launches_per_step": launches, "falsified_per_step": fails,
+                        "iters_per_pass": T / passes if passes else None}
+    return roof, launches_per_step
+
+
+def paper_engines_leg(job, K):
+    """The paper's per-iteration engines and cuda-sync without temporal blocking on
+    the same swarm (rank 0, N=1): aggregation vs blocking."""
+    cp = job.cp
+    out = {}
+    steps = max(2, min(K, 5))
+    for name in PAPER_ENGINES:
+        secs, k = job.run(2, steps, cp.find_engine(name))
+        out[name] = {"value": job.n_total * job.T * k / secs, "unit": "particle-updates/s"}
+    if job.variant == "cuda-sync":
+        os.environ["CUPSO_SYNC_MODE"] = "wave"  # read when a handle picks its mode
+        try:
+            wave = Job(cp, job.torch, None, job.dev, job.local, 1, 0, job.f.name, job.n_total, job.d, job.T,
+                       "cuda-sync", True)
+            secs, k = wave.run(2, steps)
+            wave.close()
+            out["cuda-sync (wave: one fused launch per iteration, no temporal blocking)"] = {
+                "value": job.n_total * job.T * k / secs, "unit": "particle-updates/s"}
+        finally:
+            del os.environ["CUPSO_SYNC_MODE"]
+    out["note"] = ("reduction/unrolled/queue/queue-lock: engine_reduction.hpp / engine_queue.hpp restated as one "
+                   "or two launches per iteration (CUDA graph); the queue-lock / reduction ratio is the paper's "
+                   "aggregation claim (PAPER.md:442); wave / queue-lock isolates the fused step + B200 "
+                   "aggregation; headline / wave is the temporal blocking")
+    return out
+
+
+def strong_cfg5_leg(cp, torch, pg, dev, local, world, rank, warmup, steps):
+    """BASELINE configs[4] strong-scaled: 2^28 particles in total, 2^28/N per GPU."""
+    fitness, n, d, T = STRONG
+    job = Job(cp, torch, pg, dev, local, world, rank, fitness, n, d, T, "cuda-sync", True)
+    K = max(1, min(steps, STRONG_MAX_STEPS))
+    secs, K = job.run(max(3, min(warmup, 3)), K)
+    s0, s1 = job.spec_at_start, job.sw.spec_stats()
+    rec = {"metric": "particle-updates/sec", "value": n * T * K / secs, "unit": "particle-updates/s",
+           "n_gpus": world, "steps": K, "warmup": 3, "ms_per_step": 1e3 * secs / K, "scaling": "strong",
+           "config": {"fitness": fitness, "particles_total": n, "particles_per_gpu": job.count, "dims": d,
+                      "iterations_per_step": T, "variant": "cuda-sync", "parallelism": f"dp{world} (particle shards)",
+                      "mode": job.sw.sync_mode(), "passes_per_step": (s1[0] - s0[0]) / K,
+                      "falsified_per_step": (s1[1] - s0[1]) / K},
+           "final_gbest_fit": job.sw.gbest().fit}
+    job.close()
+    return rec
+
+
+def dry_run(args, world, rank):
+    """CPU check of the launch plumbing (no GPU work): ranks, gloo rendezvous,
+    max-over-ranks reduction and the line's shape."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://", world_size=world, rank=rank)
+        import torch
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mx = float(t.item())
+        dist.destroy_process_group()
+    else:
+        mx = 1.0
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": "particle-updates/sec", "value": None, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "max_over_ranks_check": mx,
+                          "workload": args.workload,
+                          "strong_cfg5": {"dry_run": True, "n_gpus": world, "particles_total": STRONG[1],
+                                          "particles_per_gpu": STRONG[1] // world}}), flush=True)
+    return 0
 
 
 def main():
@@ -254,228 +486,107 @@ def main():
     ap.add_argument("--variant", default=None)
     ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-baseline-kernel", action="store_true")
+    ap.add_argument("--no-baseline-kernel", action="store_true", help="skip the paper_engines leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the strong_cfg5 sub-record")
+    ap.add_argument("--dry-run", action="store_true", help="launch plumbing only (CPU)")
     args = ap.parse_args()
     world, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(sys.argv[1:], args.gpus)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return dry_run(args, world, rank)
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
 
     import torch
     import paper_2205_01313_b200 as cp
 
-    local = local % max(1, torch.cuda.device_count())  # more ranks than GPUs: replicas share devices
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise RuntimeError("bench.py: no CUDA device (the product has no CPU path)")
+    local = local % ndev  # more ranks than GPUs: replicas share devices
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    fitness, n_per_rank, d, T, default_variant, desc = WORKLOADS[args.workload]
-    if args.workload == "cfg5":
-        n_total = n_per_rank
-        n_per_rank = n_total // world
-    else:
-        n_total = n_per_rank * world
+    fitness, n_base, d, T, default_variant, desc = WORKLOADS[args.workload]
     if args.iters:
         T = args.iters
-    variant_name = args.variant or default_variant
-    engine = cp.find_engine(variant_name)
-    f = cp.find_fitness(fitness)
-    p = cp.make_params(f, n_total, d, T)
-    seed = 1
-
+    variant = args.variant or default_variant
     pg = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://", world_size=world, rank=rank)
         pg = dist
-    # cuda-sync shards one swarm across the ranks (NCCL pass-record exchange);
-    # the other engines have no sharded form (cuda-async: SURVEY 8(e) "replicas
-    # only"), so at N > 1 every rank runs an independent swarm of n_per_rank
-    # particles with its own seed and no data-path collective.
-    replicas = world > 1 and variant_name != "cuda-sync"
-    if replicas:
-        p = cp.make_params(f, n_per_rank, d, T)
-        seed = 1 + rank
-        first, count = 0, n_per_rank
-    else:
-        first, count = cp.shard_range(n_total, world, rank)
 
-    def barrier():
-        if pg:
-            pg.barrier()
-        torch.cuda.synchronize()
-
-    sw = cp.Swarm(p, f, seed, device=local, first=first, count=count) if not replicas else \
-        cp.Swarm(p, f, seed, device=local)
-    if world > 1 and not replicas:
-        uid = [cp.nccl_unique_id() if rank == 0 else None]
-        pg.broadcast_object_list(uid, src=0)
-        sw.nccl_init(uid[0], world, rank)
-
-    # ---- W warmup steps, then exactly K timed steps. Each step: init_swarm and an
-    # L2 flush (untimed), then the T iterations timed with CUDA events recorded by
-    # libcupso on the stream that launches the kernels (device seconds). ----
-    for k in range(args.warmup):
-        sw.init()
-        flush_l2(torch, dev)
-        barrier()
-        sw.step(engine.variant, T)
-    per_step = []
-    spec0 = sw.spec_stats()
-    barrier()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            sw.init()
-            flush_l2(torch, dev)
-            barrier()
-            per_step.append(sw.step(engine.variant, T))
-        barrier()
+    job = Job(cp, torch, pg, dev, local, world, rank, fitness, n_base, d, T, variant, args.workload == "cfg5")
+    clk = ClockSampler(local)
+    dev_secs, K = job.run(args.warmup, args.steps, clocks=clk)
     clocks = clk.summary()
-    dev_secs = sum(per_step)
-    if pg:
-        t = torch.tensor([dev_secs], dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        dev_secs = float(t.item())
-    K = len(per_step)
-    value = n_total * T * K / dev_secs
-    gb = sw.gbest()
-    grid = sw.sync_grid_blocks()
-
-    # ---- roofline of the dominant kernel (one launch = T iterations for the persistent kernels) ----
-    f32 = variant_name == "cuda-sync-f32"
-    bytes_per_pu = (5 * d + 1) * (4 if f32 else 8)
-    # cuda-sync runs as speculative passes (k_spec: ~T/K launches per step),
-    # persistent (1 cooperative launch per step) or as a graph of one wave per
-    # iteration; shards: propose+commit per iteration
-    mode = sw.sync_mode() if variant_name == "cuda-sync" else ("spec" if f32 else None)
-    amode = sw.async_mode() if variant_name == "cuda-async" else None
-    spec1 = sw.spec_stats()
-    spec_passes = (spec1[0] - spec0[0]) / K
-    spec_launches = (spec1[2] - spec0[2]) / K
-    spec = mode in ("spec", "nccl-sharded-spec")
-    persistent = variant_name == "cuda-async" or (variant_name == "cuda-sync" and world == 1 and grid > 0
-                                                  and not spec)
-    # sharded spec: k_spec + k_spec_commit per pass (the all-gather is NCCL's)
-    launches_per_step = {"cuda-sync": (spec_launches * (2 if world > 1 else 1)) if spec else
-                         (1 if persistent else (2 * T if world > 1 else T)), "cuda-async": 1,
-                         "cuda-queue-lock": T, "cuda-queue": 2 * T, "cuda-reduction": 2 * T,
-                         "cuda-unrolled": 2 * T, "cuda-sync-f32": spec_launches}[variant_name]
-    iters_per_launch = T if persistent else (T / spec_passes if spec else 1)
-    launch_secs = (dev_secs / K) / (T / iters_per_launch)
-    alg_bytes = count * iters_per_launch * bytes_per_pu
-    peak, peak_src = measured_peak_gbs()
-    achieved = alg_bytes / launch_secs / 1e9
-    traffic, traffic_iters = ncu_traffic(args.workload, variant_name)
-    if traffic is not None and traffic_iters:
-        traffic = traffic * iters_per_launch / traffic_iters
-    sync_kernel = {"resident": f"k_sync_res<{fitness},{d if d == 1 else 0}>", "persistent": f"k_sync<{fitness}>",
-                   "wave": f"k_wave<{fitness}>", "spec": f"k_spec<{fitness},{d}>",
-                   "nccl-sharded-spec": f"k_spec<{fitness},{d}>+k_spec_commit"}.get(
-                       mode, f"k_propose<{fitness}>+k_commit")
-    if f32:
-        sync_kernel = f"k_spec32<{fitness},{d}>"
-    async_kernel = {"reg": f"k_async_reg<{fitness},{d}>", "tiled": f"k_async_tiled<{fitness}>"}.get(
-        amode, f"k_async<{fitness}>")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src,
-                "kernel": {"cuda-sync": sync_kernel, "cuda-sync-f32": sync_kernel,
-                           "cuda-async": async_kernel}.get(variant_name, f"k_classic_step<{fitness}>"),
-                "mode": mode or amode,
-                "traffic_note": "ncu dram read+write per launch (profiles/ncu_summary_r01.json); "
-                                "below alg bytes = L2-resident state, above = pbest write-backs",
-                "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_secs * 1e3,
-                "bytes_per_particle_update": bytes_per_pu}
-    # RNG ceiling: the reference's two Philox-4x32-10 calls per particle-axis alone
-    # run at 3.11e11 draw pairs/s on a B200 (profiles/micro_philox_r01.txt); the
-    # FP32 engine draws one call per particle-axis and iteration pair (4x fewer)
-    draws_ps = 3.114e11 * (4.0 if f32 else 1.0)
-    rng_peak = draws_ps / d * world  # whole job
-    roofline["rng_ceiling"] = {"bound": "issue (Philox IMAD.WIDE/LOP3)", "achieved": value,
-                               "peak": rng_peak, "unit": "particle-updates/s", "frac": value / rng_peak,
-                               "source": "profiles/micro_philox_r01.txt (draw-only microbenchmark, 1 GPU)"}
-    if spec:
-        roofline["spec"] = {"passes_per_step": spec_passes, "launches_per_step": spec_launches,
-                            "falsified_per_step": (spec1[1] - spec0[1]) / K,
-                            "iters_per_pass": T / spec_passes if spec_passes else None}
-    if mode in ("resident", "spec", "nccl-sharded-spec") or amode == "reg":
-        # The swarm lives in SMEM for the whole launch: HBM carries ~0 bytes per
-        # iteration, so the algorithmic-bytes figure above can exceed
-        # the HBM roof. The binding roof is instruction issue (Philox IMAD/LOP3 +
-        # FP64): executed warp-instructions per iteration from the committed ncu
-        # capture vs 148 SMs x 4 schedulers x SM clock.
-        e = ncu_entry(args.workload, variant_name)
-        if e.get("warp_inst_per_launch"):
-            winst_iter = e.get("warp_inst_per_iter") or e["warp_inst_per_launch"] / e["iters_per_launch"]
-            sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
-            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-            ach = winst_iter * T * K / dev_secs
-            roofline["issue_roofline"] = {
-                "bound": "issue", "achieved": ach / 1e9, "peak": nsm * 4 * sm_hz / 1e9,
-                "unit": "G warp-instructions/s", "frac": ach / (nsm * 4 * sm_hz),
-                "inst_per_particle_update": winst_iter * 32 / count,
-                "source": "smsp__inst_executed.sum of " + e.get("capture", "?")}
-        roofline["note"] = {
-            "resident": "SMEM-resident swarm (k_sync_res): state read/written once per launch, not per iteration",
-            "spec": "temporally blocked (k_spec): each pass reads/writes the state once for K iterations held in "
-                    "registers",
-            "nccl-sharded-spec": "temporally blocked shards (k_spec): one all-gather of a pass record per pass",
-        }.get(mode, "temporally blocked (k_async_reg): state read/written once per K iterations held in registers") \
-            + "; frac > 1 means the HBM model does not bind -- see issue_roofline"
+    spec0, spec1 = job.spec_at_start, job.sw.spec_stats()
+    value = job.n_total * T * K / dev_secs
+    gb = job.sw.gbest()
+    roofline, launches_per_step = roofline_of(job, args.workload, variant, dev_secs, K, clocks,
+                                              [b - a for a, b in zip(spec0, spec1)], torch)
 
     extra = {}
-    # ---- the in-repo reduction baseline kernel on the same workload (rank 0, N=1) ----
-    if world == 1 and not args.no_baseline_kernel and variant_name != "cuda-reduction":
-        red = cp.find_engine("cuda-reduction")
-        rs = []
-        for k in range(2 + max(2, args.steps // 2)):
-            sw.init()
-            flush_l2(torch, dev)
-            torch.cuda.synchronize()
-            s = sw.step(red.variant, T)
-            if k >= 2:
-                rs.append(s)
-        rv = n_total * T * len(rs) / sum(rs)
-        extra["reduction_baseline"] = {"variant": "cuda-reduction", "value": rv, "unit": "particle-updates/s",
-                                       "speedup_of_headline": value / rv}
+    if world == 1 and not args.no_baseline_kernel:
+        extra["paper_engines"] = paper_engines_leg(job, K)
+        red = extra["paper_engines"]["cuda-reduction"]["value"]
+        extra["reduction_baseline"] = {"variant": "cuda-reduction", "value": red, "unit": "particle-updates/s",
+                                       "speedup_of_headline": value / red}
 
     # ---- e2e through the reference-facing C-ABI call (cupso_run), host buffers ----
     e2e = None
-    if world == 1:
-        sw.close()  # cupso_run owns its own device swarm (cfg5: 2 x 52 GB double-buffered)
+    job.close()  # cupso_run owns its own device swarm
+    if not args.no_e2e and world == 1:
         e2e_secs = []
         for k in range(1 + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r = engine.run(p, f, cp.rng_key(seed), cp.exec_options(device=local))
+            r = job.engine.run(job.p, job.f, cp.rng_key(job.seed), cp.exec_options(device=local))
             e2e_secs.append(time.perf_counter() - t0)
         e2e_secs = e2e_secs[1:]
         h2d = C.sizeof(cp._lib.cupso_params) + 8  # params + seed; the swarm is initialised on device
         d2h = T * (8 + 4 + 8 + 8) + (16 + 8 * d) + 16  # trace, particle, admitted, async key; gbest record; initial
-        e2e = {"value": n_total * T * len(e2e_secs) / sum(e2e_secs), "unit": "particle-updates/s",
+        e2e = {"value": job.n_total * T * len(e2e_secs) / sum(e2e_secs), "unit": "particle-updates/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "cupso_run via find_engine(...).run (init_swarm + T iterations + result D2H; "
                        "device swarm reused across calls of the same shape)",
                "final_gbest_fit": r.gbest_fit}
-    else:
+    elif not args.no_e2e:
         # N > 1: the shard handle API end to end (init_swarm + NCCL gbest exchange +
         # T iterations + trace/gbest D2H), wall clock, max over ranks
+        job2 = Job(cp, torch, pg, dev, local, world, rank, fitness, n_base, d, T, variant, args.workload == "cfg5")
         e2e_secs = []
         for k in range(1 + args.steps):
-            barrier()
+            job2.barrier()
             t0 = time.perf_counter()
-            sw.init()
-            sw.step(engine.variant, T)
-            sw.trace()
-            sw.gbest()
+            job2.sw.init()
+            job2.sw.step(job2.engine.variant, T)
+            job2.sw.trace()
+            job2.sw.gbest()
             e2e_secs.append(time.perf_counter() - t0)
-        t = torch.tensor([sum(e2e_secs[1:])], dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        e2e = {"value": n_total * T * args.steps / float(t.item()), "unit": "particle-updates/s",
+        job2.close()
+        tot = job.max_over_ranks(sum(e2e_secs[1:]))
+        e2e = {"value": job.n_total * T * args.steps / tot, "unit": "particle-updates/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": T * (8 + 4 + 8 + 8) + 16 + 8 * d,
-               "path": ("Swarm API per rank (independent replicas)" if replicas else
+               "path": ("Swarm API per rank (independent replicas)" if job.replicas else
                         "Swarm shard API per rank: init (with NCCL adopt)") + " + step + trace + gbest; max over ranks"}
+
+    strong = None
+    if not args.no_strong:
+        try:
+            strong = strong_cfg5_leg(cp, torch, pg, dev, local, world, rank, args.warmup, args.steps)
+        except Exception as e:  # reported, never fatal for the headline line
+            strong = {"error": str(e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_leg(fitness, min(n_per_rank, 1 << 24), d)
+            cpu = cpu_reference_leg(fitness, min(job.count, 1 << 24), d, T)
         except Exception as e:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": "particle-updates/s", "cores": 0, "kind": "unavailable",
                    "sample": f"failed: {e}"}
@@ -484,21 +595,22 @@ def main():
         line = {
             "metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s",
             "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * dev_secs / K,
-            "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak", "vs_baseline": None,
-            "dtype": "f32" if f32 else "f64",
+            "higher_is_better": True, "scaling": "strong" if args.workload == "cfg5" else "weak",
+            "vs_baseline": None, "dtype": "f32" if variant == "cuda-sync-f32" else "f64",
             "data": "synthetic (Philox-initialised swarm, reference make_params defaults)",
-            "config": {"workload": desc, "fitness": fitness, "particles_total": n_total,
-                       "particles_per_gpu": count, "dims": d, "iterations_per_step": T,
-                       "variant": variant_name, "parallelism": f"replicas{world} (independent swarms, seeds 1..{world})" if replicas
+            "config": {"workload": desc, "fitness": fitness, "particles_total": job.n_total,
+                       "particles_per_gpu": job.count, "dims": d, "iterations_per_step": T,
+                       "variant": variant,
+                       "parallelism": f"replicas{world} (independent swarms, seeds 1..{world})" if job.replicas
                        else f"dp{world} (particle shards)",
-                       "sync_grid_blocks": grid,
-                       "l2": "flushed (512 MiB write) before every step; within a step the swarm stays resident as in a real run"},
+                       "l2": "flushed (512 MiB write) before every step; within a step the swarm stays resident "
+                             "as in a real run"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * K, "final_gbest_fit": gb.fit,
+            "strong_cfg5": strong,
             **extra,
         }
         print(json.dumps(line), flush=True)
-    sw.close()
     if pg:
         pg.destroy_process_group()
     return 0

@@ -148,7 +148,11 @@ cupso_status cupso_upload_state(cupso_swarm* h, uint32_t iteration, const double
                                 const double* velocities, const double* pbest_pos,
                                 const double* pbest_fit, double gbest_fit, uint32_t gbest_particle,
                                 const double* gbest_pos);
-/* Device pointers of the padded state (row stride = *ld elements). */
+/* Device pointers of the padded state (row stride = *ld elements). Valid until
+ * the next cupso_step / cupso_upload_state / cupso_destroy on this handle: a
+ * speculative cuda-sync step (sync mode 5/6) alternates between two state
+ * buffers and may leave the state in the other one -- call again after each
+ * step. */
 cupso_status cupso_device_state(cupso_swarm* h, double** pos, double** vel, double** pbest_pos,
                                 double** pbest_fit, uint64_t* ld);
 size_t cupso_device_bytes(const cupso_swarm* h);
@@ -236,6 +240,19 @@ cupso_status cupso_uniform01_batch(int device, uint64_t seed, const uint32_t* dr
 /* Evaluate a fitness on device for n points given axis-major (x[a*n + i]). */
 cupso_status cupso_eval_fitness(int device, int fitness_id, const double* x, uint32_t n,
                                 uint32_t dims, double* out);
+/* Concurrency self-tests, the device analogue of the reference's acceptance
+ * criterion 4 (acceptance.cpp:126-200). append: `launches` launches of
+ * 2 x SMs blocks at random group sizes 2..1024, 200 rounds each; every round
+ * a seeded subset of each block's lanes appends to the block queue and lane 0
+ * to a grid queue (queue_append, the product's append); *violations counts
+ * duplicate / missing slots and counter mismatches over *trials block-rounds.
+ * lock: lane 0 of every warp of 4 x SMs blocks increments a plain counter
+ * `iters` times under the product's spin lock (Alg. 3); *counter must equal
+ * *expected and *lock_after 0. */
+cupso_status cupso_selftest_append(int device, uint32_t launches, uint64_t seed, uint64_t* trials,
+                                   uint64_t* violations);
+cupso_status cupso_selftest_lock(int device, uint32_t iters, uint64_t* counter, uint64_t* expected,
+                                 uint32_t* lock_after);
 /* velocity_step/position_step on device for n scalar cases. */
 cupso_status cupso_eval_kinematics(int device, const cupso_params* p, const double* v,
                                    const double* x, const double* pbest_x, const double* gbest_x,

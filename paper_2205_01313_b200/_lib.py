@@ -109,6 +109,10 @@ SIGNATURES = {
     "cupso_stream": (_vp, [_vp]),
     "cupso_philox_batch": (C.c_int, [C.c_int, _up, _up, _up, C.c_size_t]),
     "cupso_uniform01_batch": (C.c_int, [C.c_int, C.c_uint64, _up, _dp, C.c_size_t]),
+    "cupso_selftest_append": (C.c_int, [C.c_int, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64)]),
+    "cupso_selftest_lock": (C.c_int, [C.c_int, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                      _up]),
     "cupso_eval_fitness": (C.c_int, [C.c_int, C.c_int, _dp, C.c_uint32, C.c_uint32, _dp]),
     "cupso_eval_kinematics": (C.c_int, [C.c_int, C.POINTER(cupso_params), _dp, _dp, _dp, _dp, _dp,
                                         _dp, _dp, _dp, C.c_size_t]),

@@ -184,6 +184,7 @@ struct cupso_swarm {
   std::vector<void*> ipc_opened;      // peer SpecCtl mappings (CUDA IPC)
   bool p2p = false;                   // pass records exchanged in-kernel over peer memory
   unsigned char* p2p_buf = nullptr;   // mailbox [2][n] records + flags [n+1]
+  uint32_t p2p_buf_n = 0;             // the shard count p2p_buf was sized for
   unsigned char* xrec_dev = nullptr;  // [xranks] gathered records on the device
   size_t xrec_cap = 0;
   unsigned char* spec_rec_local = nullptr;  // this shard's SpecRec of the running pass
@@ -692,19 +693,22 @@ cupso_status do_step(cupso_swarm* h, int variant, uint32_t iters, double* second
   // The fused kernels stage the gbest position in SMEM (<= kMaxSyncDims axes).
   // Wider swarms run the same synchronous algorithm as the classic fused
   // queue-lock launches, which read it from global memory -- bit-identical.
+  // A shard exchanging with others (NCCL, the cupso_step_exchange callback, the
+  // peer-memory mailbox, or linked early-stop hints) steps with cuda-sync only:
+  // any other variant would run its own slice and let the shards' gbest records
+  // diverge while returning OK.
+  const bool linked = h->comm || h->xfn || h->p2p || h->C.npeers > 0 || h->nranks > 1;
   if ((variant == CUPSO_SYNC || variant == CUPSO_ASYNC) && h->P.d > kMaxSyncDims) {
-    if (h->comm) return fail(CUPSO_EINVAL, "sharded cuda-sync: dims (%u) above %u", h->P.d, kMaxSyncDims);
+    if (linked) return fail(CUPSO_EINVAL, "sharded cuda-sync: dims (%u) above %u", h->P.d, kMaxSyncDims);
     variant = CUPSO_QUEUE_LOCK;
   }
   if (!h->initialized) return fail(CUPSO_ELOGIC, "cupso_step before cupso_init");
   if (static_cast<uint64_t>(h->t) + iters > h->T)
     return fail(CUPSO_EINVAL, "cupso_step: %u + %u iterations exceed max_iter (%u)", h->t, iters, h->T);
-  if (h->nranks > 1 && variant != CUPSO_SYNC)
-    return fail(CUPSO_EINVAL, "sharded swarms step with cuda-sync only");
+  if (linked && variant != CUPSO_SYNC) return fail(CUPSO_EINVAL, "sharded swarms step with cuda-sync only");
   CK(cudaSetDevice(h->device));
   const uint32_t t0 = h->t, t1 = h->t + iters;
   if (variant == CUPSO_SYNC_F32) {
-    if (h->comm) return fail(CUPSO_EINVAL, "cuda-sync-f32: sharded swarms step with cuda-sync only");
     TRY(ensure_f32(h));
     if (!h->spec_host) {
       void* host = nullptr;
@@ -1158,11 +1162,14 @@ cupso_status cupso_shard_p2p(cupso_swarm** shards, uint32_t n) {
     CK(cudaSetDevice(h->device));
     if (!spec_fits(h))
       return fail(CUPSO_EINVAL, "cupso_shard_p2p: no speculative kernel for this shape (dims %u)", h->P.d);
+    if (h->p2p_buf && h->p2p_buf_n != n)  // slots and the exchange counter are laid out for p2p_buf_n
+      return fail(CUPSO_EINVAL, "cupso_shard_p2p: shard already linked with %u shards, not %u", h->p2p_buf_n, n);
     if (!h->p2p_buf) {
       void* b;
       TRY(dmalloc(h, &b, p2p_bytes(h, n)));
       CK(cudaMemset(b, 0, p2p_bytes(h, n)));
       h->p2p_buf = static_cast<unsigned char*>(b);
+      h->p2p_buf_n = n;
     }
   }
   TRY(cupso_shard_link(shards, n));  // early-stop hints too
@@ -1595,6 +1602,64 @@ cupso_status cupso_uniform01_batch(int device, uint64_t seed, const uint32_t* dr
   k_uniform_batch<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256>>>(P, dr.p, o.p, n);
   CK(cudaGetLastError());
   CK(cudaMemcpy(out, o.p, 8 * n, cudaMemcpyDeviceToHost));
+  return CUPSO_OK;
+}
+
+cupso_status cupso_selftest_append(int device, uint32_t launches, uint64_t seed, uint64_t* trials,
+                                   uint64_t* violations) {
+  if (!trials || !violations) return fail(CUPSO_EINVAL, "cupso_selftest_append: null output");
+  CK(cudaSetDevice(device));
+  const uint32_t grid = 2u * static_cast<uint32_t>(num_sms(device)), rounds = 200;
+  const uint32_t cap = grid * rounds;
+  DevBuf<uint32_t> gq;
+  DevBuf<unsigned long long> bad;
+  CK(gq.alloc(1 + cap));
+  CK(bad.alloc(1));
+  std::vector<uint32_t> seen(1 + cap);
+  uint64_t x = seed, tr = 0, vio = 0;
+  auto next = [&x] {  // splitmix64
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  for (uint32_t l = 0; l < launches; ++l) {
+    const uint32_t gs = 2 + static_cast<uint32_t>(next() % 1023);  // group sizes 2..1024
+    const uint32_t salt = static_cast<uint32_t>(next());
+    CK(cudaMemset(gq.p, 0, 4ull * (1 + cap)));
+    CK(cudaMemset(bad.p, 0, 8));
+    k_stress_append<<<grid, gs, gs * sizeof(uint32_t)>>>(rounds, salt, gq.p, gq.p + 1, cap, bad.p);
+    CK(cudaGetLastError());
+    unsigned long long b = 0;
+    CK(cudaMemcpy(&b, bad.p, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(seen.data(), gq.p, 4ull * (1 + cap), cudaMemcpyDeviceToHost));
+    vio += b + (seen[0] != cap);
+    for (uint32_t i = 0; i < cap; ++i) vio += seen[1 + i] != 1u;
+    tr += static_cast<uint64_t>(grid) * rounds;
+  }
+  *trials = tr;
+  *violations = vio;
+  return CUPSO_OK;
+}
+
+cupso_status cupso_selftest_lock(int device, uint32_t iters, uint64_t* counter, uint64_t* expected,
+                                 uint32_t* lock_after) {
+  if (!counter || !expected || !lock_after) return fail(CUPSO_EINVAL, "cupso_selftest_lock: null output");
+  CK(cudaSetDevice(device));
+  const uint32_t grid = 4u * static_cast<uint32_t>(num_sms(device)), threads = 256;
+  DevBuf<uint32_t> lk;
+  DevBuf<unsigned long long> c;
+  CK(lk.alloc(1));
+  CK(c.alloc(1));
+  CK(cudaMemset(lk.p, 0, 4));
+  CK(cudaMemset(c.p, 0, 8));
+  k_stress_lock<<<grid, threads>>>(iters, lk.p, c.p);
+  CK(cudaGetLastError());
+  unsigned long long v = 0;
+  CK(cudaMemcpy(&v, c.p, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(lock_after, lk.p, 4, cudaMemcpyDeviceToHost));
+  *counter = v;
+  *expected = static_cast<uint64_t>(grid) * (threads / 32) * iters;
   return CUPSO_OK;
 }
 

@@ -110,61 +110,52 @@ __device__ __forceinline__ double pos_step(const KParams& P, double x, double v)
 
 // ------------------------------------------------------------- cos
 // cos(p) for the griewank / rastrigin terms (|p| <= 600 in the registered
-// boxes): Cody-Waite reduction by pi/2 with FMA, then fdlibm's minimax
-// sin/cos kernels on [-pi/4, pi/4], evaluated branch-free (both polynomials,
-// quadrant select) so a warp never diverges. ~30 FP64 instructions instead of
-// CUDA's ~100 for cos(); max error 2 ulp vs glibc over |p| <= 700 (1 ulp
-// near k*pi/2), the same class as CUDA's own cos -- the reference's glibc cos
-// is not reproducible bit for bit on the GPU either way.
-// The FP64 constants live in the constant bank: DFMA/DMUL read a c[][]
-// operand directly, whereas a 64-bit immediate costs two IMAD.MOV per use
-// (the d=32 rastrigin loop spent ~24 issue slots per cos on them).
-__constant__ double kCos[17] = {
-    0x1.8p52,                     // 0: rint shifter
-    6.36619772367581382433e-01,   // 1: 2/pi
-    1.57079632679489655800e+00,   // 2: pi/2 (Cody-Waite, 3 parts)
-    6.12323399573676603587e-17,   // 3
-    -1.49738490485916983212e-33,  // 4
-    -1.13596475577881948265e-11,  // 5: fdlibm __kernel_cos C6..C1
-    2.08757232129817482790e-09,   // 6
-    -2.75573143513906633035e-07,  // 7
-    2.48015872894767294178e-05,   // 8
-    -1.38888888888741095749e-03,  // 9
-    4.16666666666666019037e-02,   // 10
-    1.58969099521155010221e-10,   // 11: fdlibm __kernel_sin S6..S2
-    -2.50507602534068634195e-08,  // 12
-    2.75573137070700676789e-06,   // 13
-    -1.98412698298579493134e-04,  // 14
-    8.33333333332248946124e-03,   // 15
-    -1.66666666666666324348e-01,  // 16: S1
+// boxes), ONE polynomial per call: reduce by pi -- k = rint(p / pi), r = p - k*pi
+// by a 3-part Cody-Waite with FMA (exact for |k| < 2^20) -- then
+// cos(p) = (-1)^k cos(r) with |r| <= pi/2, and cos(r) = P(r^2), P the degree-8
+// Chebyshev-node interpolant of cos(sqrt z) on [0, (pi/2)^2] (max error 4e-18,
+// fitted in 80-bit long double by tools/cos_poly_fit.py). 14 FP64
+// instructions and no quadrant select, where fdlibm-style sin+cos kernels cost
+// ~30 (both polynomials, then a select). Max error 3.2e-16 absolute against
+// glibc over |p| <= 600 -- the same class as CUDA's own cos; the reference's
+// glibc cos is not reproducible bit for bit on the GPU either way (DESIGN.md
+// section 2). The FP64 constants live in the constant bank: DFMA reads a
+// c[][] operand directly, whereas a 64-bit immediate costs two IMAD.MOV per use.
+__constant__ double kCos[13] = {
+    0x1.8p52,                  // 0: rint shifter
+    0.31830988618379067154,    // 1: 1/pi
+    3.14159265358979311600e+00,  // 2: pi (Cody-Waite, 3 parts)
+    1.22464679914735317723e-16,  // 3
+    -2.99476980971833966425e-33, // 4
+    4.609001524865924e-14,     // 5: P8 .. P0 (Horner order)
+    -1.1462904621323729e-11,   // 6
+    2.087656196355758e-09,     // 7
+    -2.755731639398695e-07,    // 8
+    2.4801587277454882e-05,    // 9
+    -0.001388888888877329,     // 10
+    0.041666666666663896,      // 11
+    -0.4999999999999997,       // 12   (P0 = 1.0)
 };
-
-// fitness constants that are not 32-bit-immediate encodable (see kCos)
-__constant__ double kFitK[2] = {0.8, 6.283185307179586};
 
 __device__ __forceinline__ double cos_pso(double p) {
   const double big = kCos[0];
-  const double t = __fma_rn(p, kCos[1], big);  // rint(p * 2/pi) in the low bits
-  const double n = __dsub_rn(t, big);
-  const uint32_t q = static_cast<uint32_t>(__double2loint(t)) & 3u;
-  double r = __fma_rn(-n, kCos[2], p);
-  r = __fma_rn(-n, kCos[3], r);
-  r = __fma_rn(-n, kCos[4], r);
+  const double t = __fma_rn(p, kCos[1], big);  // rint(p / pi) in the low bits
+  const double k = __dsub_rn(t, big);
+  const uint32_t odd = static_cast<uint32_t>(__double2loint(t)) & 1u;
+  double r = __fma_rn(-k, kCos[2], p);
+  r = __fma_rn(-k, kCos[3], r);
+  r = __fma_rn(-k, kCos[4], r);
   const double z = __dmul_rn(r, r);
-  // cos kernel (fdlibm __kernel_cos, tail y = 0)
-  const double cr = __dmul_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z,
-                        kCos[5], kCos[6]), kCos[7]), kCos[8]), kCos[9]), kCos[10]));
-  const double ar = fabs(r);
-  const double qx = ar < 0.3 ? 0.0 : (ar > 0.78125 ? 0.28125 : __dmul_rn(ar, 0.25));
-  const double hz = __dsub_rn(__dmul_rn(0.5, z), qx);
-  const double kc = __dsub_rn(__dsub_rn(1.0, qx), __dsub_rn(hz, __dmul_rn(z, cr)));
-  // sin kernel (fdlibm __kernel_sin, iy = 0)
-  const double sr = __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, kCos[11], kCos[12]), kCos[13]), kCos[14]),
-                             kCos[15]);
-  const double ks = __dadd_rn(r, __dmul_rn(__dmul_rn(z, r), __fma_rn(z, sr, kCos[16])));
-  const double v = (q & 1u) ? ks : kc;
-  return (q == 1u || q == 2u) ? -v : v;
+  double c = __fma_rn(z, kCos[5], kCos[6]);
+#pragma unroll
+  for (int j = 7; j <= 12; ++j) c = __fma_rn(c, z, kCos[j]);
+  c = __fma_rn(c, z, 1.0);
+  // (-1)^k: flip the sign bit (an integer op on the high word, no select)
+  return __hiloint2double(__double2hiint(c) ^ static_cast<int>(odd << 31), __double2loint(c));
 }
+
+// fitness constants that are not 32-bit-immediate encodable (see kCos)
+__constant__ double kFitK[2] = {0.8, 6.283185307179586};
 
 // ------------------------------------------------------------- fitness
 // Accumulators fed one axis at a time in ascending order (fitness.hpp:26-27).

@@ -291,6 +291,10 @@ __device__ __forceinline__ void tree_unrolled(double* wf, uint32_t* wi, uint32_t
   }
 }
 
+// A unique slot in a block (smem) or grid (global) queue: Alg. 2 lines 1-4,
+// atomic_append (group_runtime.hpp:182-187). Pinned by k_stress_append.
+__device__ __forceinline__ uint32_t queue_append(uint32_t* count) { return atomicAdd(count, 1u); }
+
 // Global spin lock (Alg. 3 atomicCAS(lock,0,1) / atomicExch(lock,0); group_runtime.hpp:190-205).
 __device__ __forceinline__ void lock_acquire(uint32_t* lock) {
   const uint64_t t0 = globaltimer_ns();
@@ -344,7 +348,7 @@ __global__ void k_classic_step(KParams P, KState S, KCtl C, uint32_t t, uint32_t
   } else {
     const double snap_fit = C.snap->fit;
     if (active && fit > snap_fit) {  // Alg. 2 lines 1-4: conditional atomic append
-      const uint32_t slot = atomicAdd(&s_n, 1u);
+      const uint32_t slot = queue_append(&s_n);
       wf[slot] = fit;
       wi[slot] = P.base + li;
     }
@@ -459,7 +463,7 @@ __global__ void k_classic_fold(KParams P, KState S, KCtl C, uint32_t t, uint32_t
     if (lane == 0) s_n = 0;
     __syncthreads();
     if (mf > snap_fit) {
-      const uint32_t slot = atomicAdd(&s_n, 1u);
+      const uint32_t slot = queue_append(&s_n);
       wf[slot] = mf;
       wi[slot] = mi;
     }
@@ -837,7 +841,7 @@ __device__ __forceinline__ void sync_arrive(const KParams& P, const KCtl& C, uin
     uint32_t i = lane < nq ? sh.bc.i[lane] : kNoParticle;
     warp_argmax(f, i);
     uint32_t slot = 0;
-    if (lane == 0) slot = atomicAdd(&C.q_count[qb], 1u);
+    if (lane == 0) slot = queue_append(&C.q_count[qb]);
     slot = __shfl_sync(0xffffffffu, slot, 0);
     const size_t e = static_cast<size_t>(qb) * cap + slot;
     if (lane == 0) {
@@ -908,7 +912,7 @@ __device__ __forceinline__ void sync_tail(const KParams& P, const KCtl& C, uint3
       uint32_t i = lane < nq ? sh.bc.i[lane] : kNoParticle;
       warp_argmax(f, i);
       uint32_t slot = 0;
-      if (lane == 0) slot = atomicAdd(&C.q_count[qb], 1u);
+      if (lane == 0) slot = queue_append(&C.q_count[qb]);
       slot = __shfl_sync(0xffffffffu, slot, 0);
       const size_t e = static_cast<size_t>(qb) * cap + slot;
       if (lane == 0) {
@@ -1198,7 +1202,7 @@ __global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_wave(KParams 
       uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
       warp_argmax(f, i);
       uint32_t slot = 0;
-      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
+      if (lane == 0) slot = queue_append(&C.q_count[0]);
       slot = __shfl_sync(0xffffffffu, slot, 0);
       if (lane == 0) {
         C.q_fit[slot] = f;
@@ -1267,7 +1271,7 @@ __global__ void __launch_bounds__(kSyncThreads, CFG::kMinBlocks) k_propose(KPara
       uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
       warp_argmax(f, i);
       uint32_t slot = 0;
-      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
+      if (lane == 0) slot = queue_append(&C.q_count[0]);
       slot = __shfl_sync(0xffffffffu, slot, 0);
       if (lane == 0) {
         C.q_fit[slot] = f;
@@ -1647,6 +1651,57 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_async_tiled(KParams P, KSta
       for (uint32_t j = tid; j < m; j += blockDim.x) S.pbf[s0 + j] = spbf[j];
       __syncthreads();  // the next tile overwrites SMEM
     }
+  }
+}
+
+
+// ------------------------------------------------ concurrency self-tests
+// Device analogue of the reference's acceptance criterion 4
+// (acceptance.cpp:126-200), run through cupso_selftest_*.
+// (a) append uniqueness: every round, the lanes selected by
+// ((lane ^ salt) + round) % 4 != 0 append to the block queue with
+// queue_append; the claimed slots must be exactly 0..count-1, each once, and
+// the counter must equal the number of appenders. Lane 0 of every block also
+// appends once per round to a grid queue (unique over the whole grid,
+// checked on the host).
+__global__ void k_stress_append(uint32_t rounds, uint32_t salt, uint32_t* gq_count, uint32_t* gq_seen,
+                                uint32_t gq_cap, unsigned long long* violations) {
+  extern __shared__ uint32_t seen[];
+  __shared__ uint32_t s_n;
+  const uint32_t tid = threadIdx.x;
+  uint32_t bad = 0;
+  for (uint32_t round = 0; round < rounds; ++round) {
+    seen[tid] = 0;
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    const bool app = ((tid ^ salt) + round) % 4u != 0u;
+    const uint32_t slot = app ? queue_append(&s_n) : kNoParticle;
+    if (app) {
+      if (slot < blockDim.x) atomicAdd(&seen[slot], 1u);
+      else ++bad;
+    }
+    const uint32_t want = static_cast<uint32_t>(__syncthreads_count(app));
+    if (tid == 0 && s_n != want) ++bad;
+    if (seen[tid] != (tid < want ? 1u : 0u)) ++bad;
+    if (tid == 0) {
+      const uint32_t g = queue_append(gq_count);
+      if (g < gq_cap) atomicAdd(&gq_seen[g], 1u);
+    }
+    __syncthreads();
+  }
+  if (bad) atomicAdd(violations, static_cast<unsigned long long>(bad));
+}
+
+// (b) lock exclusion: lane 0 of every warp increments a plain (non-atomic,
+// volatile) counter `iters` times under lock_acquire / lock_release; any lost
+// update shows as a counter below warps * iters.
+__global__ void k_stress_lock(uint32_t iters, uint32_t* lock, unsigned long long* counter) {
+  if ((threadIdx.x & 31u) != 0) return;
+  volatile unsigned long long* c = counter;
+  for (uint32_t i = 0; i < iters; ++i) {
+    lock_acquire(lock);
+    *c = *c + 1ull;
+    lock_release(lock);
   }
 }
 

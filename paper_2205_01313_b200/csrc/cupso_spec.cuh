@@ -219,7 +219,7 @@ __device__ __forceinline__ void spec_finish(const KParams& P, const KState& So, 
       uint32_t i = lane < nq ? bc.i[lane] : kNoParticle;
       warp_argmax(f, i);
       uint32_t slot = 0;
-      if (lane == 0) slot = atomicAdd(&C.q_count[0], 1u);
+      if (lane == 0) slot = queue_append(&C.q_count[0]);
       slot = __shfl_sync(0xffffffffu, slot, 0);
       if (lane == 0) {
         C.q_fit[slot] = f;
@@ -640,14 +640,18 @@ namespace cupso {
 //   * before the unit's K iterations the warp takes a consistent copy of the
 //     live record (seqlock: even version, unchanged after the copy; skipped
 //     when the version did not move);
-//   * during them the thread only counts admissions (f > its view) into
-//     admitted[t], and an admitted particle becomes the thread's own view of
-//     the gbest (fit and position) -- no polling, no warp collectives in the
-//     iteration loop;
-//   * after them the warp's best pbest that beats the view (beats() order, warp
-//     ballot + shuffle argmax) is published by its lane with the CAS(version
-//     even->odd) protocol of async_commit, and folded into trace_key[t] at the
-//     iteration it was found.
+//   * during them the thread counts admissions (f > its view) into admitted[t],
+//     and an admitted particle becomes the thread's own view of the gbest (fit
+//     and position);
+//   * at an iteration where some lane of the warp made a find, the warp's best
+//     new pbest (beats() order, warp ballot + shuffle argmax) is published by
+//     its lane with the CAS(version even->odd) protocol of async_commit and
+//     folded into trace_key[t];
+//   * every iteration the warp compares the live record's version (a relaxed
+//     load issued before the step, so its latency hides behind the arithmetic)
+//     with the one it holds and re-reads the record when it moved, so particles
+//     move against the latest published gbest, as in the paper's asynchronous
+//     variant, while their state stays in registers for K iterations.
 // Lanes past the end of the swarm run the loop with neutral state so every
 // warp-collective sees all 32 lanes.
 // Out-of-line slow paths of k_async_reg: keeping them out of the iteration
@@ -659,12 +663,16 @@ namespace cupso {
 __device__ __noinline__ uint32_t areg_refresh(const KCtl& C, uint32_t d, uint32_t gver, double* slot,
                                              uint64_t ts) {
   const uint32_t lane = threadIdx.x & 31;
+  (void)ts;
+  uint64_t spin0 = 0;  // the timeout counts from the first wait, not from the kernel's start
   for (;;) {
     uint32_t v = 0;
     if (lane == 0) v = ld_acquire_gpu(C.seq);
     v = __shfl_sync(0xffffffffu, v, 0);
     if (v & 1u) {  // a writer holds the record: back off instead of hammering its L2 line
-      if (globaltimer_ns() - ts > kSpinTimeoutNs) __trap();
+      const uint64_t now = globaltimer_ns();
+      if (!spin0) spin0 = now;
+      else if (now - spin0 > kSpinTimeoutNs) __trap();
       __nanosleep(200);
       continue;
     }
@@ -764,8 +772,11 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KSt
         }
       }
       bool dirty = false;
-      uint32_t tfound = 0;  // iteration of this thread's latest admission
       for (uint32_t t = tb; t < te; ++t) {
+        // the live record's version, read now and compared after the step: the
+        // load's latency hides behind the iteration's arithmetic
+        uint32_t vnow = 0;
+        if (lane == 0) vnow = ld_relaxed_gpu(C.seq);
         Fit<F> acc[NP];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -807,45 +818,58 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KSt
             }
           }
         }
-        if (adm) {  // rare after warm-up; one atomic per warp
-          const unsigned m = __activemask();
-          const uint32_t wadm = __reduce_add_sync(m, adm);
+        // Publish at the iteration of the find: the warp's best new pbest
+        // (beats() order, ballot + shuffle argmax) goes to the live record by
+        // the CAS(version even->odd) protocol of async_commit -- a block
+        // publishes only when it improved the gbest (north_star), and rarely
+        // after warm-up, so the common iteration pays one ballot.
+        if (__any_sync(0xffffffffu, adm != 0)) {
+          const unsigned m = __ballot_sync(0xffffffffu, adm != 0);
+          const uint32_t wadm = __reduce_add_sync(0xffffffffu, adm);
           if (lane == static_cast<uint32_t>(__ffs(m) - 1))
             atomicAdd(&C.admitted[t], static_cast<unsigned long long>(wadm));
-          tfound = t;
-        }
-      }
-      // Publish: the unit's pbests that beat the view are gbest candidates
-      // (the gbest is the max of all pbests); the warp's best in beats()
-      // order goes to the live record once per unit instead of per iteration.
-      double bf = -INFINITY;
-      uint32_t bi = kNoParticle, bk = 0;
-      const double view = slot[0];  // the unit's starting view (gfit may hold own finds)
+          double bf = -INFINITY;
+          uint32_t bi = kNoParticle, bk = 0;
+          const double view = slot[0];  // the last consistent copy of the live record
 #pragma unroll
-      for (int k = 0; k < NP; ++k)
-        if (ok[k] && pbf[k] > view && beats(pbf[k], g0 + k, bf, bi)) {
-          bf = pbf[k];
-          bi = g0 + k;
-          bk = k;
-        }
-      if (__any_sync(0xffffffffu, bi != kNoParticle)) {
-        double wf = bf;
-        uint32_t wi = bi;
-        warp_argmax(wf, wi);
-        __syncwarp();
-        if (bi == wi && bi != kNoParticle) {  // the winning lane publishes
+          for (int k = 0; k < NP; ++k)
+            if (ok[k] && pbf[k] > view && beats(pbf[k], g0 + k, bf, bi)) {
+              bf = pbf[k];
+              bi = g0 + k;
+              bk = k;
+            }
+          double wf = bf;
+          uint32_t wi = bi;
+          warp_argmax(wf, wi);
+          __syncwarp();
+          if (bi == wi && bi != kNoParticle) {  // the winning lane publishes
 #pragma unroll
-          for (int a = 0; a < D; ++a) {
-            double pa = pb[a][0];
+            for (int a = 0; a < D; ++a) {
+              double pa = pb[a][0];
 #pragma unroll
-            for (int k = 1; k < NP; ++k)
-              if (bk == static_cast<uint32_t>(k)) pa = pb[a][k];
-            s_pub[warp][a] = pa;
+              for (int k = 1; k < NP; ++k)
+                if (bk == static_cast<uint32_t>(k)) pa = pb[a][k];
+              s_pub[warp][a] = pa;
+            }
+            const double seen = areg_publish(C, D, wf, wi, s_pub[warp], view);
+            atomicMax(&C.trace_key[t], order_key(seen));
           }
-          const double seen = areg_publish(C, D, wf, wi, s_pub[warp], view);
-          atomicMax(&C.trace_key[tfound], order_key(seen));
+          __syncwarp();
+          vnow = ~gver;  // re-read the record below (ours, or the one that beat it)
         }
-        __syncwarp();
+        // Re-read the live record when its version moved: every particle then
+        // moves against the latest published gbest at the next iteration, while
+        // its state stays in registers for the whole K-iteration unit.
+        vnow = __shfl_sync(0xffffffffu, vnow, 0);
+        if (vnow != gver) {
+          gver = areg_refresh(C, D, gver, slot, ts);
+          const double lf = slot[0];
+          if (!(gfit > lf)) {  // never step back from this thread's own find
+            gfit = lf;
+#pragma unroll
+            for (int a = 0; a < D; ++a) gp[a] = slot[1 + a];
+          }
+        }
       }
       if (live) {
 #pragma unroll

@@ -260,7 +260,10 @@ def _make_entry(v: int) -> engine_entry:
     def run(p, f, key, opts=None, observe=None, _v=v):
         return run_cuda(p, f, key if isinstance(key, rng_key) else rng_key(int(key)), _v, opts, observe)
 
-    return engine_entry(name, True, run, bool(lib().cupso_variant_deterministic(v)), v)
+    # parallel means "bitwise equal to run_serial" in the reference's acceptance
+    # (acceptance.cpp:57-59), as in the C++ adapter: not cuda-async / cuda-sync-f32
+    det = bool(lib().cupso_variant_deterministic(v))
+    return engine_entry(name, det, run, det, v)
 
 
 def engine_registry() -> list[engine_entry]:

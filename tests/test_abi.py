@@ -55,7 +55,8 @@ def test_abi_version_and_registry(cupso):
     engines = cupso.engine_registry()
     assert [e.name for e in engines] == ["cuda-reduction", "cuda-unrolled", "cuda-queue",
                                          "cuda-queue-lock", "cuda-sync", "cuda-async", "cuda-sync-f32"]
-    assert all(e.parallel for e in engines)
+    # parallel = bitwise equal to run_serial (acceptance.cpp:57-59), as the C++ adapter sets it
+    assert [e.parallel for e in engines] == [True] * 5 + [False, False]
     assert [e.deterministic for e in engines] == [True] * 5 + [False, False]
     assert cupso.find_engine("sync").name == "cuda-sync"  # short names accepted
 

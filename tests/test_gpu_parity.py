@@ -242,12 +242,12 @@ def test_golden_reference_runs(cupso):
 
 # ---------------------------------------------------- acceptance criteria
 def test_acceptance_cross_engine_equivalence(cupso, oracle):
-    """acceptance.cpp:40-76 for the CUDA engines (3 of its 5 seeds to bound runtime)."""
+    """acceptance.cpp:40-76 for the CUDA engines, the reference's 5 seeds (acceptance.cpp:47)."""
     f = cupso.find_fitness("cubic")
     runs = 0
     for n in (33, 128, 256, 1024):
         for d in (1, 120):
-            for seed in (11, 22, 33):
+            for seed in (11, 22, 33, 44, 55):
                 base = oracle.run_serial("cubic", n, d, 100, seed, want_state=False)
                 for gs in (32, 128):
                     p = cupso.make_params(f, n, d, 100, gs)
@@ -256,7 +256,7 @@ def test_acceptance_cross_engine_equivalence(cupso, oracle):
                         assert_bitwise(r.trace, base.trace, f"{e} n={n} d={d} gs={gs} seed={seed}")
                         assert_bitwise(r.gbest_pos, base.gbest_pos, f"{e} gbest_pos")
                         runs += 1
-    assert runs == 4 * 2 * 3 * 2 * len(DET_ENGINES)
+    assert runs == 4 * 2 * 5 * 2 * len(DET_ENGINES)
 
 
 @pytest.mark.parametrize("engine", DET_ENGINES + ["cuda-async"])

@@ -175,3 +175,32 @@ def test_oracle_shard_step_replays_serial(oracle):
     ref = oracle.run_serial(f, n, d, T, seed)
     assert np.array_equal(bits(trace), bits(ref.trace))
     assert np.array_equal(bits(gpos), bits(ref.gbest_pos))
+
+
+@pytest.mark.parametrize("case", ["cfg2", "cfg5proxy", "cfg5long", "cfg4"])
+def test_full_size_fixtures_consistent(oracle, case):
+    """The full-length reference fixtures (tests/golden/make_full_golden.py) are
+    self-consistent, and the cfg2 one carries the survey's own checksum."""
+    path = os.path.join(HERE, "golden", f"full_{case}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = np.load(path)
+    n, d, T = int(g["particles"]), int(g["dims"]), int(g["iters"])
+    tr = g["trace"]
+    assert tr.shape == (T,) and g["trace_particle"].shape == (T,)
+    assert (np.diff(tr) >= 0).all() and tr[-1] == g["gbest_fit"]
+    assert g["trace_particle"][-1] == g["gbest_particle"]
+    assert oracle.checksum(tr) == str(g["checksum"])
+    # the gbest particle is in the sample: its pbest is the gbest record
+    k = int(np.nonzero(g["sample_idx"] == g["gbest_particle"])[0][0])
+    assert g["sample_pbest_fit"][0, k] == g["gbest_fit"]
+    assert bits(g["sample_pbest_pos"][:, k]).tolist() == bits(g["gbest_pos"]).tolist()
+    # sampled particles' stored fitness is the oracle's fitness of their position
+    fit = str(g["fitness"])
+    for j in range(0, len(g["sample_idx"]), 97):
+        got = oracle.fitness(fit, g["sample_positions"][:, j])
+        want = g["sample_fitness"][0, j]
+        assert got == want if fit != "rastrigin" else abs(got - want) <= 1e-12 * max(1.0, abs(want))
+    if case == "cfg2":
+        assert str(g["checksum"]) == "585d124f8e33b353"  # SURVEY.md 8c, seed 1 at N=1024 and N=2^20 alike
+        assert n == 1 << 20 and d == 1 and T == 1000

@@ -73,7 +73,7 @@ def test_bench_reference_arm_contract():
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=root)
+                          "--warmup", "1", "--iters", "20"], capture_output=True, text=True, timeout=300, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["metric"] == "particle-updates/sec"
@@ -82,3 +82,38 @@ def test_bench_reference_arm_contract():
     assert cpu["kind"] in ("reference", "port") and cpu["cores"] >= 1 and cpu["sample"]
     assert cpu["value"] == line["value"]
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
+    # a step fitting the budget runs the workload's whole T (same config as the GPU arm)
+    assert line["config"]["same_config"] is True and line["config"]["iterations_per_step"] == 20
+
+
+def test_bench_spawns_ranks_for_gpus_n():
+    """`bench.py --gpus 2` outside torchrun starts 2 ranks itself (torch.distributed.run,
+    127.0.0.1); rank 0 prints the line with n_gpus 2 and the strong_cfg5 sub-record.
+    --dry-run exercises the launch plumbing (gloo, max over ranks) without a GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                          "--steps", "2", "--warmup", "3"], capture_output=True, text=True, timeout=300,
+                         cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["max_over_ranks_check"] == 2.0
+    assert line["strong_cfg5"]["particles_per_gpu"] == (1 << 28) // 2
+
+
+def test_bench_rejects_world_mismatch():
+    """Under torchrun, --gpus must equal WORLD_SIZE (a silent 1-rank run is an error)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "8", "--dry-run"],
+                         capture_output=True, text=True, timeout=120, cwd=root, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr
