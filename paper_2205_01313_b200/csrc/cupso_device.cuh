@@ -178,6 +178,9 @@ struct Fit<kCubic> {  // fitness.hpp:47-54
   }
   __device__ __forceinline__ void accum(Term t, double, uint32_t) { acc = __dadd_rn(acc, t); }
   __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
+  // axis 0 of a fresh accumulator: 0.0 + t == t bit for bit unless t is -0.0,
+  // and the term's last operation (+ 8000) cannot round to -0.0
+  __device__ __forceinline__ void add_first(double v) { acc = term(v, 0); }
   __device__ __forceinline__ double value() const { return acc; }
   __device__ __forceinline__ void shfl_up(unsigned m, int w) { acc = __shfl_up_sync(m, acc, 1, w); }
 };
@@ -189,6 +192,7 @@ struct Fit<kSphere> {  // fitness.hpp:57-61
   __device__ __forceinline__ static Term term(double v, uint32_t) { return __dmul_rn(v, v); }
   __device__ __forceinline__ void accum(Term t, double, uint32_t) { acc = __dadd_rn(acc, t); }
   __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
+  __device__ __forceinline__ void add_first(double v) { acc = term(v, 0); }  // v*v is never -0.0
   __device__ __forceinline__ double value() const { return -acc; }
   __device__ __forceinline__ void shfl_up(unsigned m, int w) { acc = __shfl_up_sync(m, acc, 1, w); }
 };
@@ -208,6 +212,7 @@ struct Fit<kRosenbrock> {  // fitness.hpp:65-73: pairs (x_d, x_{d+1}) in ascendi
     prev = v;
   }
   __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
+  __device__ __forceinline__ void add_first(double v) { prev = v; }
   __device__ __forceinline__ double value() const { return -acc; }
   __device__ __forceinline__ void shfl_up(unsigned m, int w) {
     acc = __shfl_up_sync(m, acc, 1, w);
@@ -230,6 +235,12 @@ struct Fit<kGriewank> {  // fitness.hpp:77-85 (cos_pso: <= 2 ulp from glibc)
     prod = __dmul_rn(prod, t.c);
   }
   __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
+  // 0.0 + v*v/4000 (never -0.0) and 1.0 * c are exact identities
+  __device__ __forceinline__ void add_first(double v) {
+    const Term t = term(v, 0);
+    sum = t.s;
+    prod = t.c;
+  }
   __device__ __forceinline__ double value() const { return -__dsub_rn(__dadd_rn(1.0, sum), prod); }
   __device__ __forceinline__ void shfl_up(unsigned m, int w) {
     sum = __shfl_up_sync(m, sum, 1, w);
@@ -246,6 +257,7 @@ struct Fit<kRastrigin> {  // harness fitness_fn (oracle/pso_oracle.c:rastrigin)
   }
   __device__ __forceinline__ void accum(Term t, double, uint32_t) { acc = __dadd_rn(acc, t); }
   __device__ __forceinline__ void add(double v, uint32_t a) { accum(term(v, a), v, a); }
+  __device__ __forceinline__ void add_first(double v) { acc = term(v, 0); }  // (...) + 10 is never -0.0
   __device__ __forceinline__ double value() const { return -acc; }
   __device__ __forceinline__ void shfl_up(unsigned m, int w) { acc = __shfl_up_sync(m, acc, 1, w); }
 };

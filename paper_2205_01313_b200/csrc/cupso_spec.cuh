@@ -336,7 +336,10 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
           const double r2 = uniform53(P, t, g0 + k, a, 1);
           v[a][k] = vel_step53(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
           x[a][k] = pos_step(P, x[a][k], v[a][k]);
-          acc[k].add(x[a][k], a);
+          if (a == 0)
+            acc[k].add_first(x[a][k]);  // unrolled: a is a constant
+          else
+            acc[k].add(x[a][k], a);
         }
       }
       // Fast path: no particle improved its pbest. The snapshot is the max of
@@ -786,7 +789,10 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KSt
             const double r2 = uniform53(P, t, g0 + k, a, 1);
             v[a][k] = vel_step53(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
             x[a][k] = pos_step(P, x[a][k], v[a][k]);
-            acc[k].add(x[a][k], a);
+            if (a == 0)
+              acc[k].add_first(x[a][k]);  // unrolled: a is a constant
+            else
+              acc[k].add(x[a][k], a);
           }
         }
         uint32_t adm = 0;
