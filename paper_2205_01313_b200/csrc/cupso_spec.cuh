@@ -428,8 +428,9 @@ __device__ __forceinline__ uint32_t warp_tmin(const uint32_t* tmin) {
 // of registers -- fewer live registers, so more resident warps and no spills
 // for the cos-heavy fitnesses; dynamic SMEM = (3 + term width) * DL * blockDim
 // doubles.
-// RAGGED: the swarm's d is below DL * G (any d up to 256): lane s holds the
-// valid axes of [s*DL, s*DL + DL) and skips the rest (warp-uniform tests).
+// RAGGED: the swarm's d is below DL * G (any d up to 256): lane s holds axes
+// [s*dl, s*dl + dl), dl = ceil(d / G) <= DL, and skips the slots past d
+// (warp-uniform tests).
 // PBSM = 1: only the pbest columns live in shared memory (DL * blockDim
 // doubles): read once per axis-iteration (one LDS), written on the rare
 // improvement. PBSM = 2: the velocity columns too (one LDS + one STS more).
@@ -462,12 +463,15 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec_split(KParams P, KS
   const uint32_t t0 = s_ctl[0], K = s_ctl[1], par = s_ctl[2];
   if (t0 >= t_end) return;
   const bool inplace = K == 1;
-  auto valid = [&](int a) { return !RAGGED || sub * DL + a < P.d; };
+  // RAGGED: the d axes spread evenly over the G lanes, ceil(d / G) <= DL each
+  // (d = 12: 6 + 6 instead of 8 + 4 -- the slowest lane sets the pace)
+  const uint32_t dl = RAGGED ? (P.d + G - 1) / G : DL;
+  auto valid = [&](int a) { return !RAGGED || (static_cast<uint32_t>(a) < dl && sub * dl + a < P.d); };
   const KState Si = par ? S1 : S0;
   const KState So = inplace ? Si : (par ? S0 : S1);
   const double snap_fit = C.snap->fit;
   const uint32_t tl = t0 + K - 1;
-  const uint32_t a0 = sub * DL;  // first axis of this lane
+  const uint32_t a0 = sub * dl;  // first axis of this lane
   // the gbest position is read from SMEM at each use (broadcast LDS): holding
   // its 8 doubles in registers cost spills (cfg4: 2.7 % slower)
   double bf = -INFINITY;
@@ -889,6 +893,151 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_async_reg(KParams P, KSt
           for (int a = 0; a < D; ++a) stv<NP>(S.pb + static_cast<size_t>(a) * ld + li, pb[a]);
           stv<NP>(S.pbf + li, pbf);
         }
+      }
+    }
+  }
+}
+
+
+// ------------------------------------------- async, register-resident, wide
+// cuda-async for d above 8 (up to 256): k_spec_split's lane layout (G lanes
+// per particle, DL axes per lane, the ordered shfl_up fold) with k_async_reg's
+// asynchronous protocol -- K iterations per unit with the state in registers,
+// a find published at its iteration by the warp's best group (CAS-seqlock),
+// the live record's version checked every iteration. Dynamic SMEM: two private
+// columns per lane (pbest and this particle's view of the gbest), DL x
+// blockDim doubles each; the warp's consistent copy of the live record and the
+// publisher's position are static.
+template <int F, int DL, int G, int MINB, bool RAGGED>
+__global__ void __launch_bounds__(kSyncThreads, MINB) k_async_split(KParams P, KState S, KCtl C, uint32_t t0,
+                                                                   uint32_t t1, uint32_t K) {
+  constexpr int D = DL * G;
+  static_assert(32 % G == 0, "G must divide the warp");
+  extern __shared__ double s_cols[];  // [0, DL): pbest columns, [DL, 2 DL): view columns
+  __shared__ double s_slot[kSyncWarps][1 + D];
+  __shared__ double s_pub[kSyncWarps][D];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane % G;
+  const uint32_t dl = RAGGED ? (P.d + G - 1) / G : DL;  // balanced ragged split, as k_spec_split
+  const uint32_t bd = blockDim.x, a0 = sub * dl;
+  double* slot = s_slot[warp];
+  const uint64_t ts = globaltimer_ns();
+  uint32_t gver = 0xffffffffu;
+  auto valid = [&](int a) { return !RAGGED || (static_cast<uint32_t>(a) < dl && a0 + a < P.d); };
+  auto PB = [&](int a) -> double& { return s_cols[a * bd + tid]; };
+  auto GV = [&](int a) -> double& { return s_cols[(DL + a) * bd + tid]; };
+  const uint32_t stride = gridDim.x * (blockDim.x / G);
+  const size_t ld = P.ld;
+  for (uint32_t tb = t0; tb < t1; tb += K) {
+    const uint32_t te = min(tb + K, t1);
+    for (uint32_t u0 = (blockIdx.x * blockDim.x + (tid & ~31u)) / G; u0 < P.n; u0 += stride) {
+      gver = areg_refresh(C, P.d, gver, slot, ts);  // the latest published gbest for this unit
+      double gfit = slot[0];
+#pragma unroll
+      for (int a = 0; a < DL; ++a) GV(a) = valid(a) ? slot[1 + a0 + a] : 0.0;
+      const uint32_t li = u0 + lane / G;
+      const bool live = li < P.n;
+      const uint32_t gi = P.base + li;
+      double rx[DL], rv[DL], pbf = -INFINITY;
+#pragma unroll
+      for (int a = 0; a < DL; ++a) {
+        if (!live || !valid(a)) {
+          rx[a] = rv[a] = PB(a) = 0.0;
+          continue;
+        }
+        const size_t at = static_cast<size_t>(a0 + a) * ld + li;
+        rx[a] = S.pos[at];
+        rv[a] = S.vel[at];
+        PB(a) = S.pb[at];
+      }
+      if (live) pbf = S.pbf[li];
+      bool dirty = false;
+      for (uint32_t t = tb; t < te; ++t) {
+        uint32_t vnow = 0;
+        if (lane == 0) vnow = ld_relaxed_gpu(C.seq);  // consumed after the step
+        Fit<F> acc;
+        typename Fit<F>::Term tm[DL];
+        double xs[F == kRosenbrock ? DL : 1];
+#pragma unroll
+        for (int a = 0; a < DL; ++a) {
+          if (!valid(a)) continue;
+          const double r1 = uniform53(P, t, gi, a0 + a, 0);
+          const double r2 = uniform53(P, t, gi, a0 + a, 1);
+          const double x0 = rx[a];
+          const double nv = vel_step53(P, rv[a], x0, PB(a), GV(a), r1, r2);
+          const double nx = pos_step(P, x0, nv);
+          rv[a] = nv;
+          rx[a] = nx;
+          tm[a] = Fit<F>::term(nx, a0 + a);
+          if constexpr (F == kRosenbrock) xs[a] = nx;
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {  // ordered fold across the group
+          if (q > 0) acc.shfl_up(0xffffffffu, G);
+          if (sub == static_cast<uint32_t>(q)) {
+#pragma unroll
+            for (int a = 0; a < DL; ++a)
+              if (valid(a)) acc.accum(tm[a], F == kRosenbrock ? xs[a] : 0.0, a0 + a);
+          }
+        }
+        const double f = __shfl_sync(0xffffffffu, acc.value(), G - 1, G);
+        if (live && f > pbf) {  // update_pbest (swarm.hpp:100-108)
+          dirty = true;
+          pbf = f;
+#pragma unroll
+          for (int a = 0; a < DL; ++a) PB(a) = rx[a];
+        }
+        bool find = false;
+        if (live && f > gfit) {  // beats this particle's view: it becomes the view
+          find = true;
+          gfit = f;
+#pragma unroll
+          for (int a = 0; a < DL; ++a) GV(a) = rx[a];
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, find && sub == 0);
+        if (fm) {  // publish at the iteration of the find (rare after warm-up)
+          if (lane == static_cast<uint32_t>(__ffs(fm) - 1))
+            atomicAdd(&C.admitted[t], static_cast<unsigned long long>(__popc(fm)));
+          const double view = slot[0];  // the last consistent copy of the live record
+          const bool cand = sub == 0 && live && pbf > view;
+          double wf = cand ? pbf : -INFINITY;
+          uint32_t wi = cand ? gi : kNoParticle;
+          warp_argmax(wf, wi);
+          if (wi != kNoParticle) {
+            if (gi == wi) {  // the winning group's lanes stage its pbest position
+#pragma unroll
+              for (int a = 0; a < DL; ++a)
+                if (valid(a)) s_pub[warp][a0 + a] = PB(a);
+            }
+            __syncwarp();
+            if (gi == wi && sub == 0) {
+              const double seen = areg_publish(C, P.d, wf, wi, s_pub[warp], view);
+              atomicMax(&C.trace_key[t], order_key(seen));
+            }
+            __syncwarp();
+          }
+          vnow = ~gver;  // re-read the record below
+        }
+        vnow = __shfl_sync(0xffffffffu, vnow, 0);
+        if (vnow != gver) {
+          gver = areg_refresh(C, P.d, gver, slot, ts);
+          const double lf = slot[0];
+          if (!(gfit > lf)) {  // never step back from this particle's own find
+            gfit = lf;
+#pragma unroll
+            for (int a = 0; a < DL; ++a) GV(a) = valid(a) ? slot[1 + a0 + a] : 0.0;
+          }
+        }
+      }
+      if (live) {
+#pragma unroll
+        for (int a = 0; a < DL; ++a) {
+          if (!valid(a)) continue;
+          const size_t at = static_cast<size_t>(a0 + a) * ld + li;
+          S.pos[at] = rx[a];
+          S.vel[at] = rv[a];
+          if (dirty) S.pb[at] = PB(a);
+        }
+        if (dirty && sub == 0) S.pbf[li] = pbf;
       }
     }
   }

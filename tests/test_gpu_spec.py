@@ -272,3 +272,39 @@ def test_async_throughput_floor(cupso):
         s = sw.step(cupso.ASYNC, 60)
         assert sw.async_mode() == "reg"
     assert (1 << 24) * 60 / s > 1.2e11, f"{(1 << 24) * 60 / s:.3e} p-u/s"
+
+
+@pytest.mark.parametrize("n,d,want", [(32768, 120, "spec"), (65536, 120, "wave"), (70000, 100, "wave"),
+                                      (1 << 20, 64, "spec"), (1 << 17, 256, "wave")])
+def test_wide_swarm_mode_choice(cupso, n, d, want):
+    """Above 64 dims the pass kernel runs only for swarms below 65536 particles:
+    larger ones are faster as one k_wave launch per iteration."""
+    f = cupso.find_fitness("sphere")
+    p = cupso.make_params(f, n, d, 2)
+    with cupso.Swarm(p, f, 3) as sw:
+        sw.step(cupso.SYNC, 2)
+        assert sw.sync_mode() == want
+
+
+@pytest.mark.parametrize("fit,d", [("rastrigin", 32), ("sphere", 12), ("griewank", 100), ("rosenbrock", 64),
+                                   ("cubic", 256), ("sphere", 3)])
+def test_async_split_kernel_invariants(cupso, oracle, fit, d):
+    """cuda-async above 8 dims (and at 3/5/6/7) runs k_async_split (registers, G lanes per
+    particle): monotone trace, a self-consistent gbest record equal to the best pbest."""
+    f = cupso.find_fitness(fit)
+    n, T = 3001, 70
+    p = cupso.make_params(f, n, d, T)
+    with cupso.Swarm(p, f, 5) as sw:
+        sw.step(cupso.ASYNC, 30)
+        sw.step(cupso.ASYNC, T - 30)
+        assert sw.async_mode() == "reg"
+        tr, _, _ = sw.trace()
+        gb = sw.gbest()
+        st = sw.state()
+    assert (np.diff(tr) >= 0).all() and tr[-1] == gb.fit
+    assert st.pbest_fit.max() == gb.fit and st.pbest_fit[gb.particle] == gb.fit
+    pos = st.pbest_pos.reshape(d, n)[:, gb.particle]
+    assert np.array_equal(pos.view(np.uint64), np.asarray(gb.pos).view(np.uint64))
+    want = oracle.fitness(fit, gb.pos)
+    assert abs(want - gb.fit) <= 1e-12 * max(1.0, abs(want))
+    assert (st.positions >= p.min_pos).all() and (st.positions <= p.max_pos).all()
