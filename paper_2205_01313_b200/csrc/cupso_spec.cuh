@@ -266,6 +266,112 @@ __device__ __forceinline__ void spec_finish(const KParams& P, const KState& So, 
   }
 }
 
+// One thread unit of a pass: NP adjacent particles from li, K iterations in
+// registers against the snapshot (the iteration loop of k_spec). Returns false
+// when the pass has already failed at t0 (nothing left to compute).
+template <int F, int D, int NP>
+__device__ __forceinline__ bool spec_unit(const KParams& P, const KState& Si, const KState& So, const KCtl& C,
+                                          SpecCtl* sc, uint32_t li, uint32_t t0, uint32_t K, bool inplace,
+                                          double snap_fit, const double (&gp)[D], uint32_t& tstop, double& bf,
+                                          uint32_t& bi, uint32_t& adm) {
+  const uint32_t tl = t0 + K - 1;  // the only iteration whose admissions stand
+  const size_t ld = P.ld;
+  tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+  uint32_t te = min(t0 + K, tstop);  // iterations >= tstop cannot change the outcome
+  if (te <= t0) return false;        // the pass already failed at t0
+  const uint32_t g0 = P.base + li;
+  double x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
+  bool ok[NP];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const size_t at = static_cast<size_t>(a) * ld + li;
+    ldv<NP>(Si.pos + at, x[a]);
+    ldv<NP>(Si.vel + at, v[a]);
+    ldv<NP>(Si.pb + at, pb[a]);
+  }
+  ldv<NP>(Si.pbf + li, pbf);
+#pragma unroll
+  for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
+  uint32_t t = t0;
+  bool bad = false;
+  bool dirty = false;  // some pbest of this unit changed
+  for (; t < te; ++t) {
+    Fit<F> acc[NP];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const double r1 = uniform53(P, t, g0 + k, a, 0);
+        const double r2 = uniform53(P, t, g0 + k, a, 1);
+        v[a][k] = vel_step53(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
+        x[a][k] = pos_step(P, x[a][k], v[a][k]);
+        if (a == 0)
+          acc[k].add_first(x[a][k]);  // unrolled: a is a constant
+        else
+          acc[k].add(x[a][k], a);
+      }
+    }
+    // Fast path: no particle improved its pbest. The snapshot is the max of
+    // the pbests when the pass starts and an admission before the last
+    // iteration ends it, so f > snapshot implies f > pbest: one compare per
+    // particle decides the common case (nothing to do) in a single branch.
+    double fv[NP];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      fv[k] = acc[k].value();
+      any |= ok[k] && fv[k] > pbf[k];
+    }
+    if (any) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const double f = fv[k];
+        if (!ok[k]) continue;
+        if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
+          dirty = true;
+          pbf[k] = f;
+#pragma unroll
+          for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+        }
+        if (f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
+          if (t < tl) {
+            bad = true;
+          } else {
+            ++adm;
+            if (beats(f, g0 + k, bf, bi)) {
+              bf = f;
+              bi = g0 + k;
+            }
+          }
+        }
+      }
+      if (bad) {
+        spec_falsify(C, &sc->tmin, t);
+        tstop = t;
+        break;
+      }
+    }
+    if (((t - t0) & 15u) == 15u) {
+      tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+      te = min(te, tstop);
+    }
+  }
+  if (!bad && t == t0 + K) {  // completed the pass: commit this unit to B
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const size_t at = static_cast<size_t>(a) * ld + li;
+      stv<NP>(So.pos + at, x[a]);
+      stv<NP>(So.vel + at, v[a]);
+    }
+    if (!inplace || dirty) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) stv<NP>(So.pb + static_cast<size_t>(a) * ld + li, pb[a]);
+      stv<NP>(So.pbf + li, pbf);
+    }
+  }
+  return true;
+}
+
 // D: dims (compile time; the particle's whole state lives in registers).
 // NP: adjacent particles per thread unit (2: LDG.128 / STG.128 on every row).
 template <int F, int D, int NP, int MINB>
@@ -297,109 +403,34 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec(KParams P, KState S
   const KState Si = par ? S1 : S0;
   const KState So = inplace ? Si : (par ? S0 : S1);
   const double snap_fit = C.snap->fit;
-  const uint32_t tl = t0 + K - 1;  // the only iteration whose admissions stand
   double gp[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) gp[a] = s_gpos[a];
   double bf = -INFINITY;
   uint32_t bi = kNoParticle, adm = 0;
   uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
-  const uint32_t units = (P.n + NP - 1) / NP;
-  const size_t ld = P.ld;
-  for (uint32_t u = blockIdx.x * blockDim.x + tid; u < units; u += gridDim.x * blockDim.x) {
-    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
-    uint32_t te = min(t0 + K, tstop);  // iterations >= tstop cannot change the outcome
-    if (te <= t0) break;               // the pass already failed at t0
-    const uint32_t li = NP * u, g0 = P.base + li;
-    double x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
-    bool ok[NP];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const size_t at = static_cast<size_t>(a) * ld + li;
-      ldv<NP>(Si.pos + at, x[a]);
-      ldv<NP>(Si.vel + at, v[a]);
-      ldv<NP>(Si.pb + at, pb[a]);
-    }
-    ldv<NP>(Si.pbf + li, pbf);
-#pragma unroll
-    for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
-    uint32_t t = t0;
-    bool bad = false;
-    bool dirty = false;  // some pbest of this unit changed
-    for (; t < te; ++t) {
-      Fit<F> acc[NP];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const double r1 = uniform53(P, t, g0 + k, a, 0);
-          const double r2 = uniform53(P, t, g0 + k, a, 1);
-          v[a][k] = vel_step53(P, v[a][k], x[a][k], pb[a][k], gp[a], r1, r2);
-          x[a][k] = pos_step(P, x[a][k], v[a][k]);
-          if (a == 0)
-            acc[k].add_first(x[a][k]);  // unrolled: a is a constant
-          else
-            acc[k].add(x[a][k], a);
-        }
-      }
-      // Fast path: no particle improved its pbest. The snapshot is the max of
-      // the pbests when the pass starts and an admission before the last
-      // iteration ends it, so f > snapshot implies f > pbest: one compare per
-      // particle decides the common case (nothing to do) in a single branch.
-      double fv[NP];
-      bool any = false;
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        fv[k] = acc[k].value();
-        any |= ok[k] && fv[k] > pbf[k];
-      }
-      if (any) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const double f = fv[k];
-          if (!ok[k]) continue;
-          if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
-            dirty = true;
-            pbf[k] = f;
-#pragma unroll
-            for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
-          }
-          if (f > snap_fit) {  // snapshot filter (engine_queue.hpp:91)
-            if (t < tl) {
-              bad = true;
-            } else {
-              ++adm;
-              if (beats(f, g0 + k, bf, bi)) {
-                bf = f;
-                bi = g0 + k;
-              }
-            }
-          }
-        }
-        if (bad) {
-          spec_falsify(C, &sc->tmin, t);
-          tstop = t;
-          break;
-        }
-      }
-      if (((t - t0) & 15u) == 15u) {
-        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
-        te = min(te, tstop);
-      }
-    }
-    if (!bad && t == t0 + K) {  // completed the pass: commit this unit to B
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const size_t at = static_cast<size_t>(a) * ld + li;
-        stv<NP>(So.pos + at, x[a]);
-        stv<NP>(So.vel + at, v[a]);
-      }
-      if (!inplace || dirty) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) stv<NP>(So.pb + static_cast<size_t>(a) * ld + li, pb[a]);
-        stv<NP>(So.pbf + li, pbf);
-      }
-    }
+  // Rounds of NP-particle units over the grid; when the last round would be
+  // at most half full, its particles go to one round of NP/2-particle units
+  // instead, so every thread finishes after the same work (2^20 d = 1 on 148
+  // SMs x 512 threads: 3.46 rounds of 4 -> 3 rounds of 4 + 1 of 2).
+  const uint32_t nthr = gridDim.x * blockDim.x, gt = blockIdx.x * blockDim.x + tid;
+  constexpr bool kTail = NP >= 2 && (NP / 2 == 1 || (NP / 2) % 2 == 0);  // ldv: 1 or even
+  uint32_t n_main = P.n;
+  if constexpr (kTail) {
+    const uint32_t per_round = NP * nthr;
+    const uint32_t rem = P.n % per_round;
+    if (rem && rem <= (NP / 2) * nthr) n_main = P.n - rem;
+  }
+  const uint32_t units = (n_main + NP - 1) / NP;
+  bool live = true;
+  for (uint32_t u = gt; u < units; u += nthr) {
+    if (!(live = spec_unit<F, D, NP>(P, Si, So, C, sc, NP * u, t0, K, inplace, snap_fit, gp, tstop, bf, bi, adm)))
+      break;
+  }
+  if constexpr (kTail) {
+    const uint32_t li = n_main + (NP / 2) * gt;
+    if (live && li < P.n)
+      spec_unit<F, D, NP / 2>(P, Si, So, C, sc, li, t0, K, inplace, snap_fit, gp, tstop, bf, bi, adm);
   }
   spec_finish<D>(P, So, C, sc, s_ctl, bc, rs, s_last, t_end, kmax, snap_fit, bf, bi, adm, rec_out, sharded);
 }

@@ -308,3 +308,21 @@ def test_async_split_kernel_invariants(cupso, oracle, fit, d):
     want = oracle.fitness(fit, gb.pos)
     assert abs(want - gb.fit) <= 1e-12 * max(1.0, abs(want))
     assert (st.positions >= p.min_pos).all() and (st.positions <= p.max_pos).all()
+
+
+@pytest.mark.parametrize("fit,n,d", [("cubic", 934003, 1), ("sphere", 1048576, 1), ("rosenbrock", 308105, 2),
+                                     ("sphere", 606209, 1)])
+def test_spec_tail_round_matches_oracle(cupso, oracle, spec_env, fit, n, d):
+    """k_spec's last grid round in half-size units (3 rounds of 4 particles + 1
+    of 2 at 2^20 d = 1 on 148 SMs): the tail units, their ragged end and the
+    main/tail boundary stay bit-identical to run_serial."""
+    T, seed = 40, 23
+    got = run_sync(cupso, fit, n, d, T, seed)
+    assert got["mode"] == "spec"
+    orc = oracle.run_serial(fit, n, d, T, seed)
+
+    class R:
+        trace, trace_particle = got["trace"], got["trace_particle"]
+        gbest_pos, gbest_particle = got["gbest"].pos, got["gbest"].particle
+    compare_run(R, orc, fit, f"tail {fit} n={n} d={d}")
+    compare_state(got["state"], orc, fit, f"tail {fit} n={n}")
