@@ -26,7 +26,11 @@ paper_engines: the paper's per-iteration engines (reduction, unrolled, queue,
           queue-lock) and cuda-sync without temporal blocking (wave mode) on the
           same workload, so the gain splits into aggregation and blocking.
 strong_cfg5: BASELINE configs[4] as a strong-scaling sub-record on every line:
-          sphere d=8, 2^28 particles in total, 2^28/N per GPU.
+          sphere d=8, 2^28 particles in total, 2^28/N per GPU (+ the reduction
+          kernel on the same swarm at N=1).
+other_workloads: BASELINE configs[2] (cfg3, cuda-async) and configs[3] (cfg4,
+          cuda-sync) timed in the same run at N=1, each with its roof and the
+          reduction kernel on the same swarm.
 cpu_baseline: the unmodified reference (oracle/_ref, queue-lock engine, all
           host threads) on a bounded sample of the same workload, rank 0 only.
 Multi-GPU: `--gpus N` without WORLD_SIZE re-launches itself under
@@ -386,6 +390,14 @@ def roofline_of(job, workload, variant, dev_secs, K, clocks, spec_delta, torch):
                 "inst_per_particle_update": e["warp_inst_per_step"] * 32 / (job.count * T),
                 "peak_source": f"{nsm} SMs x 4 schedulers x SM clock {sm_hz / 1e6:.0f} MHz (NVML, timed region)",
                 "source": f"smsp__inst_executed.sum over the exact timed schedule ({e.get('capture', '?')})"}
+    if roof is not None and e.get("fmaheavy_cycles_per_step"):
+        # the pipe Philox saturates: IMAD.WIDE.U32 holds the fma-heavy pipe 4 cycles per
+        # warp-instruction per SMSP (tools/micro/pipes.cu); busy SMSP-cycles of the exact
+        # schedule (ncu) over the live SMSP-cycles of the timed region
+        busy = e["fmaheavy_cycles_per_step"] * K
+        roof["pipe_fmaheavy"] = {"frac": busy / (4 * nsm * sm_hz * dev_secs),  # .sum counts per SMSP "busy_smsp_cycles_per_step":
+                                 e["fmaheavy_cycles_per_step"], "ncu_pct_of_active": e.get("fmaheavy_pct_of_active_ncu"),
+                                 "source": "sm__pipe_fmaheavy_cycles_active.sum over the exact timed schedule"}
     if roof is None:  # streaming kernels: the HBM model binds
         roof = dict(hbm, traffic=traffic)
     roof.update({"kernel": kernel, "mode": mode or amode, "hbm_model": hbm,
@@ -450,8 +462,45 @@ def strong_cfg5_leg(cp, torch, pg, dev, local, world, rank, warmup, steps):
                       "mode": job.sw.sync_mode(), "passes_per_step": (s1[0] - s0[0]) / K,
                       "falsified_per_step": (s1[1] - s0[1]) / K},
            "final_gbest_fit": job.sw.gbest().fit}
+    if world == 1:  # the in-repo reduction kernel on the same 2^28 swarm (~4 s per step)
+        rsecs, rk = job.run(1, 2, cp.find_engine("cuda-reduction"))
+        red = n * T * rk / rsecs
+        rec["reduction_baseline"] = {"variant": "cuda-reduction", "value": red, "unit": "particle-updates/s",
+                                     "speedup": rec["value"] / red}
     job.close()
     return rec
+
+
+def workload_leg(cp, torch, dev, local, name, warmup, steps):
+    """Another BASELINE workload on the same GPU in the same run (rank 0, N=1):
+    its default engine, timed exactly like the headline (device time, L2
+    flushed, clocks sampled), its binding roof, and the in-repo reduction kernel
+    on the same swarm -- so every configs[] row is measured by the driver's own
+    bench run, not only the headline."""
+    fitness, n, d, T, variant, desc = WORKLOADS[name]
+    job = Job(cp, torch, None, dev, local, 1, 0, fitness, n, d, T, variant, True)
+    try:
+        clk = ClockSampler(local)
+        secs, K = job.run(max(3, min(warmup, 3)), max(2, min(steps, 5)), clocks=clk)
+        clocks = clk.summary()
+        s0, s1 = job.spec_at_start, job.sw.spec_stats()
+        roof, launches = roofline_of(job, name, variant, secs, K, clocks, [b - a for a, b in zip(s0, s1)], torch)
+        value = n * T * K / secs
+        rsecs, rk = job.run(1, 2, cp.find_engine("cuda-reduction"))
+        red = n * T * rk / rsecs
+        keep = ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "mode", "inst_per_particle_update",
+                "pipe_fmaheavy")
+        return {"metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s", "steps": K,
+                "ms_per_step": 1e3 * secs / K, "dtype": "f64",
+                "config": {"workload": desc, "fitness": fitness, "particles": n, "dims": d,
+                           "iterations_per_step": T, "variant": variant},
+                "roofline": {k: v for k, v in roof.items() if k in keep},
+                "hbm_model_frac": roof["hbm_model"]["frac"], "clocks": clocks, "gpu_launches": launches * K,
+                "reduction_baseline": {"variant": "cuda-reduction", "value": red, "unit": "particle-updates/s",
+                                       "speedup": value / red},
+                "final_gbest_fit": job.sw.gbest().fit}
+    finally:
+        job.close()
 
 
 def dry_run(args, world, rank):
@@ -489,6 +538,7 @@ def main():
     ap.add_argument("--no-baseline-kernel", action="store_true", help="skip the paper_engines leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-strong", action="store_true", help="skip the strong_cfg5 sub-record")
+    ap.add_argument("--no-others", action="store_true", help="skip the cfg3 / cfg4 sub-records")
     ap.add_argument("--dry-run", action="store_true", help="launch plumbing only (CPU)")
     args = ap.parse_args()
     world, rank, local = dist_env()
@@ -583,6 +633,15 @@ def main():
         except Exception as e:  # reported, never fatal for the headline line
             strong = {"error": str(e)}
 
+    others = None
+    if world == 1 and args.workload == "cfg2" and not args.no_others:
+        others = {}
+        for name in ("cfg3", "cfg4"):
+            try:
+                others[name] = workload_leg(cp, torch, dev, local, name, args.warmup, args.steps)
+            except Exception as e:  # reported, never fatal for the headline line
+                others[name] = {"error": str(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -608,6 +667,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * K, "final_gbest_fit": gb.fit,
             "strong_cfg5": strong,
+            "other_workloads": others,
             **extra,
         }
         print(json.dumps(line), flush=True)

@@ -22,7 +22,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-METRICS = "dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,gpu__time_duration.sum"
+METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,gpu__time_duration.sum,"
+           "sm__pipe_fmaheavy_cycles_active.sum,sm__pipe_fp64_cycles_active.sum,sm__pipe_alu_cycles_active.sum,"
+           "sm__cycles_active.sum,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active")
 KERNELS = {  # variant -> kernel regex of its timed launches
     "cuda-sync": "k_spec|k_wave|k_sync|k_propose|k_commit",
     "cuda-async": "k_async",
@@ -37,10 +39,10 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "Kinst"
 
 def capture(tag, workload, variant):
     csv_path = os.path.join(OUT, f"ncu_bench_{tag}_{workload}_{variant}.csv")
-    cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "-k", f"regex:{KERNELS[variant]}", "--csv",
+    cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "--replay-mode", "application", "-k", f"regex:{KERNELS[variant]}", "--csv",
            "--log-file", csv_path, sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload,
            "--variant", variant, "--steps", "1", "--warmup", "0", "--no-cpu", "--no-baseline-kernel", "--no-e2e",
-           "--no-strong"]
+           "--no-strong", "--no-others"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=3000)
     if r.returncode != 0:
         print(r.stdout[-2000:], r.stderr[-2000:])
@@ -83,6 +85,16 @@ def main():
             "dram_read_per_step": tot["dram__bytes_read.sum"], "dram_write_per_step": tot["dram__bytes_write.sum"],
             "warp_inst_per_step": tot["smsp__inst_executed.sum"],
             "kernel_ms_per_step_ncu": tot["gpu__time_duration.sum"],
+            # SM-cycles per step each pipe was busy (summed over SMs) and SM-active cycles:
+            # the fma-heavy pipe runs IMAD/IMAD.WIDE (Philox), 4 cycles per IMAD.WIDE.U32
+            # warp-instruction per SMSP on sm_100a (tools/micro/pipes.cu)
+            "fmaheavy_cycles_per_step": tot.get("sm__pipe_fmaheavy_cycles_active.sum"),
+            "fp64_cycles_per_step": tot.get("sm__pipe_fp64_cycles_active.sum"),
+            "alu_cycles_per_step": tot.get("sm__pipe_alu_cycles_active.sum"),
+            "sm_active_cycles_per_step": tot.get("sm__cycles_active.sum"),
+            "fmaheavy_pct_of_active_ncu": sum(x.get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", 0)
+                                              * x.get("sm__cycles_active.sum", 0) for x in ls)
+            / max(1.0, tot.get("sm__cycles_active.sum", 0.0)),
             "bench_ms_per_step_under_ncu": line["ms_per_step"],
             "capture": f"profiles/ncu_bench_{tag}_{wl}_{var}.csv (tools/ncu_bench.py: one bench.py step, "
                        f"--metrics {METRICS}, --clock-control none)",
