@@ -395,8 +395,9 @@ def roofline_of(job, workload, variant, dev_secs, K, clocks, spec_delta, torch):
         # warp-instruction per SMSP (tools/micro/pipes.cu); busy SMSP-cycles of the exact
         # schedule (ncu) over the live SMSP-cycles of the timed region
         busy = e["fmaheavy_cycles_per_step"] * K
-        roof["pipe_fmaheavy"] = {"frac": busy / (4 * nsm * sm_hz * dev_secs),  # .sum counts per SMSP "busy_smsp_cycles_per_step":
-                                 e["fmaheavy_cycles_per_step"], "ncu_pct_of_active": e.get("fmaheavy_pct_of_active_ncu"),
+        roof["pipe_fmaheavy"] = {"frac": busy / (4 * nsm * sm_hz * dev_secs),  # the .sum counts per SMSP
+                                 "busy_smsp_cycles_per_step": e["fmaheavy_cycles_per_step"],
+                                 "ncu_pct_of_active": e.get("fmaheavy_pct_of_active_ncu"),
                                  "source": "sm__pipe_fmaheavy_cycles_active.sum over the exact timed schedule"}
     if roof is None:  # streaming kernels: the HBM model binds
         roof = dict(hbm, traffic=traffic)
