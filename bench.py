@@ -363,7 +363,8 @@ def roofline_of(job, workload, variant, dev_secs, K, clocks, spec_delta, torch):
     achieved = alg_bytes / launch_secs / 1e9
     fit = job.f.name
     kernel = {"resident": f"k_sync_res<{fit},{d}>", "persistent": f"k_sync<{fit}>", "wave": f"k_wave<{fit}>",
-              "spec": f"k_spec<{fit},{d}>", "nccl-sharded-spec": f"k_spec<{fit},{d}>+k_spec_commit"}.get(
+              "spec": f"k_spec<{fit},{d}>" if d in (1, 2, 4, 8) and not (fit == "rastrigin" and d == 8)
+              else f"k_spec_split<{fit},d={d}>", "nccl-sharded-spec": f"k_spec<{fit},{d}>+k_spec_commit"}.get(
                   mode, f"k_propose<{fit}>+k_commit")
     if f32:
         kernel = f"k_spec32<{fit},{d}>"
