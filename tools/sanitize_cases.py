@@ -18,6 +18,9 @@ CASES = [  # (fitness, n, d, T, variant, env)
     ("rosenbrock", 2001, 17, 20, cp.SYNC_F32, {}),   # k_spec32_split, ragged
     ("rastrigin", 1001, 32, 20, cp.SYNC_F32, {}),    # k_spec32_split 8 x 4
     ("griewank", 999, 300, 5, cp.SYNC_F32, {}),      # k_wave32 (d > 256)
+    ("cubic", 700001, 1, 5, cp.SYNC, {"CUPSO_SYNC_MODE": "spec"}),   # k_spec NP=4 + the NP=2 tail round
+    ("sphere", 300001, 2, 5, cp.SYNC, {"CUPSO_SYNC_MODE": "spec"}),  # k_spec NP=2 + the NP=1 tail round
+    ("griewank", 777, 12, 20, cp.ASYNC, {"CUPSO_ASYNC_MODE": "reg"}),  # k_async_split, ragged
 ]
 which = sys.argv[1:] and [int(x) for x in sys.argv[1].split(",")] or range(len(CASES))
 for k in which:
