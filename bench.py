@@ -205,14 +205,34 @@ def _reference_runner():
 
 
 def cpu_reference_leg(fitness, n, d, T, max_seconds=12.0):
-    """The reference on a bounded sample of the workload (~max_seconds)."""
+    """The reference on a bounded sample of the workload (~max_seconds), plus its
+    other CPU engines (serial on 1 core, reduction on all host
+    cores) on ~3 s samples each."""
     kind, threads, run, engine = _reference_runner()
     per_iter = max(run(fitness, n, d, 2) / 2, 1e-6)
     iters = max(2, min(T, int(max_seconds / per_iter)))
     secs = run(fitness, n, d, iters)
-    return {"value": n * iters / secs, "unit": "particle-updates/s", "cores": threads, "kind": kind,
-            "sample": f"{engine}: {fitness} d={d}, {n} particles x {iters} of {T} iterations "
-                      f"(compute loop {secs:.2f} s, seed 1, cpu={_cpu_model()})"}
+    out = {"value": n * iters / secs, "unit": "particle-updates/s", "cores": threads, "kind": kind,
+           "sample": f"{engine}: {fitness} d={d}, {n} particles x {iters} of {T} iterations "
+                     f"(compute loop {secs:.2f} s, seed 1, cpu={_cpu_model()})"}
+    if kind == "reference":
+        import oracle as orc
+        ref = orc.Reference()
+        engines = {}
+        for name, thr in (("serial", 1), ("reduction", threads)):
+            try:
+                def go(it):
+                    r, _ = ref.run(name, fitness, n, d, it, 1, threads=thr, want_particles=False)
+                    return r.compute_seconds
+                pi = max(go(2) / 2, 1e-6)
+                it = max(2, min(T, int(3.0 / pi)))
+                sec = go(it)
+                engines[f"{name} ({thr} thread{'s' if thr > 1 else ''})"] = {
+                    "value": n * it / sec, "unit": "particle-updates/s", "iterations": it}
+            except Exception as e:  # reported, never fatal
+                engines[name] = {"error": str(e)}
+        out["other_engines"] = engines
+    return out
 
 
 def run_reference_arm(args, world, rank):
