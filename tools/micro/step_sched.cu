@@ -1,0 +1,129 @@
+// Microbenchmark: instruction-scheduling variants of k_spec's d = 1 iteration
+// body (NP = 4 cubic particles per thread, the reference's two Philox draws per
+// particle, vel/pos step with clamps, cubic fitness, pbest compare), to test
+// whether mixing the IMAD.WIDE-bound Philox with the FP64/select work inside a
+// warp raises fma-heavy pipe utilisation. Compile like the library
+// (-fmad=false). Run: ./step_sched
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../paper_2205_01313_b200/csrc/cupso_device.cuh"
+using namespace cupso;
+
+constexpr int NP = 4;
+
+__device__ __forceinline__ void fence_block(uint32_t t) {
+  // a block boundary ptxas cannot schedule across (never taken)
+  if (t == 0xfffffff0u) asm volatile("trap;");
+}
+
+template <int V>
+__global__ void __launch_bounds__(256, 2) k(KParams P, double* out, uint32_t iters, double g) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g0 = NP * u;
+  double x[NP], v[NP], pb[NP], pbf[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    x[k] = 0.001 * (g0 + k);
+    v[k] = 0.0;
+    pb[k] = x[k];
+    pbf[k] = 1e300;
+  }
+  uint32_t hits = 0;
+  for (uint32_t t = 0; t < iters; ++t) {
+    double f[NP];
+    if constexpr (V == 0) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const double r1 = uniform53(P, t, g0 + k, 0, 0), r2 = uniform53(P, t, g0 + k, 0, 1);
+        v[k] = vel_step53(P, v[k], x[k], pb[k], g, r1, r2);
+        x[k] = pos_step(P, x[k], v[k]);
+        Fit<kCubic> a;
+        a.add_first(x[k]);
+        f[k] = a.value();
+      }
+    } else {
+      // V1: two halves; the second half's Philox shares a block with the first half's kinematics
+      double r1[NP], r2[NP];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        r1[k] = uniform53(P, t, g0 + k, 0, 0);
+        r2[k] = uniform53(P, t, g0 + k, 0, 1);
+      }
+      fence_block(t);
+#pragma unroll
+      for (int k = 2; k < 4; ++k) {
+        r1[k] = uniform53(P, t, g0 + k, 0, 0);
+        r2[k] = uniform53(P, t, g0 + k, 0, 1);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        v[k] = vel_step53(P, v[k], x[k], pb[k], g, r1[k], r2[k]);
+        x[k] = pos_step(P, x[k], v[k]);
+        Fit<kCubic> a;
+        a.add_first(x[k]);
+        f[k] = a.value();
+      }
+      fence_block(t + 1);
+#pragma unroll
+      for (int k = 2; k < 4; ++k) {
+        v[k] = vel_step53(P, v[k], x[k], pb[k], g, r1[k], r2[k]);
+        x[k] = pos_step(P, x[k], v[k]);
+        Fit<kCubic> a;
+        a.add_first(x[k]);
+        f[k] = a.value();
+      }
+    }
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) any |= f[k] > pbf[k];
+    if (any) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (f[k] > pbf[k]) {
+          pbf[k] = f[k];
+          pb[k] = x[k];
+          ++hits;
+        }
+    }
+  }
+  double s = hits;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) s += x[k] + v[k] + pb[k];
+  out[u] = s;
+}
+
+template <int V>
+void run(const char* name, const KParams& P, double* out, int nsm) {
+  const int grid = 2 * nsm;
+  const uint32_t iters = 4000;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k<V><<<grid, 256>>>(P, out, 10, 0.5);
+  cudaEventRecord(a);
+  k<V><<<grid, 256>>>(P, out, iters, 0.5);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("%-28s %.3f ms  %.3e particle-updates/s\n", name, ms, double(grid) * 256 * NP * iters / (ms * 1e-3));
+}
+
+int main() {
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  KParams P{};
+  P.w = 1.0; P.c1 = 2.0; P.c2 = 2.0;
+  P.min_pos = -10; P.max_pos = 10; P.min_v = -10; P.max_v = 10;
+  P.c1s = 2.0 * 0x1.0p-53; P.c2s = 2.0 * 0x1.0p-53; P.scaled_ok = 1;
+  uint32_t a = 1, b = 0;
+  for (int r = 0; r < 10; ++r) { P.k0[r] = a; P.k1[r] = b; a += 0x9E3779B9u; b += 0xBB67AE85u; }
+  double* out;
+  cudaMalloc(&out, 148 * 2 * 256 * 8 * 4);
+  for (int rep = 0; rep < 2; ++rep) {
+    run<0>("V0 straight (k_spec body)", P, out, nsm);
+    run<1>("V1 halves, mixed blocks", P, out, nsm);
+  }
+  return 0;
+}
