@@ -10,7 +10,8 @@ selection ("all" = every CUDA engine), trimmed mean over --repeat runs with
 the determinism audit, the frozen CSV schema, the speedup table (baseline
 engine --baseline, default cuda-reduction since the reference's "serial" is
 the CPU), the paper sweeps (--sweep 1d|120d, --paper-scale), and
---occupancy-out. --device selects the GPU.
+--occupancy-out. --device selects the GPU; --devices N shards cuda-sync over N
+GPUs of this process (the reference's --devices wish).
 """
 from __future__ import annotations
 
@@ -65,6 +66,9 @@ def main(argv=None) -> int:
     ap.add_argument("--from-csv", default=None, help="render the table from an existing CSV and exit")
     ap.add_argument("--occupancy-out", default=None, help="write per-iteration queue occupancy (first seed)")
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--devices", default=None,
+                    help="shard cuda-sync over several GPUs of this process: a count N (GPUs 0..N-1) or a "
+                         "comma-separated device list; the trajectory is the single-GPU one")
     a = ap.parse_args(argv)
 
     if a.from_csv:
@@ -84,6 +88,13 @@ def main(argv=None) -> int:
         return 2
     if a.baseline not in engines:
         engines = [a.baseline] + engines
+    devices = None
+    if a.devices:
+        devices = (tuple(range(int(a.devices))) if "," not in a.devices
+                   else tuple(int(x) for x in a.devices.split(",")))
+        if len(devices) > 1 and any(e != "cuda-sync" for e in engines if e != a.baseline):
+            print("error: --devices shards cuda-sync only", file=sys.stderr)
+            return 2
     seeds = a.seed or [1]
     cells = ([(a.particles, a.iters)] if not a.sweep else
              (sweep_1d if a.sweep == "1d" else sweep_120d)(a.paper_scale))
@@ -93,7 +104,8 @@ def main(argv=None) -> int:
         for e in engines:
             cfg = protocol.bench_config(engine=e, particles=particles, dims=dims, iters=iters,
                                         group_size=a.group_size, seeds=seeds, repeat=a.repeat,
-                                        fitness=a.fitness, out_path=a.out, device=a.device)
+                                        fitness=a.fitness, out_path=a.out, device=a.device,
+                                        devices=devices if e == "cuda-sync" else None)
             for rec in protocol.run_bench(cfg):
                 print_record(rec)
                 records.append(rec)

@@ -149,11 +149,16 @@ class rng_key:
 @dataclass
 class exec_options:
     """group_runtime.hpp:217-222. threads / jitter have no GPU meaning and are
-    accepted for signature compatibility; `device` selects the GPU."""
+    accepted for signature compatibility; `device` selects the GPU. `devices`
+    (the device-list knob SURVEY 8(b) asks for): shard one cuda-sync swarm over
+    these GPUs in this process -- contiguous global particle ranges, the pass
+    records exchanged over peer memory inside the pass kernel -- with a
+    trajectory bit-identical to the single-GPU run."""
     threads: int = 0
     contexts_per_group: int = 0
     schedule_jitter: Optional[Callable] = None
     device: int = 0
+    devices: Optional[tuple] = None
 
 
 # ----------------------------------------------------------------- results
@@ -202,6 +207,8 @@ def run_cuda(p: pso_params, f: fitness_fn, key: rng_key, variant: int,
     """The engine_fn body: one full run on the GPU through cupso_run."""
     opts = opts or exec_options()
     p.validate()
+    if opts.devices is not None and len(opts.devices) > 1:
+        return run_sharded(p, f, key, variant, tuple(int(x) for x in opts.devices), observe)
     cp = p.to_c()
     T, d = p.max_iter, p.dims
     gpos = np.zeros(d)
@@ -240,6 +247,68 @@ def run_cuda(p: pso_params, f: fitness_fn, key: rng_key, variant: int,
     check(st)
     return run_result(res.gbest_fit, gpos, res.gbest_particle, res.initial_gbest_fit, trace,
                       res.compute_seconds, occ if res.has_occupancy else np.zeros(0), tp)
+
+
+def run_sharded(p: pso_params, f: fitness_fn, key: rng_key, variant: int, devices: tuple,
+                observe: Optional[iteration_observer] = None) -> run_result:
+    """cuda-sync with the swarm sharded over several GPUs of this process
+    (exec_options.devices): shard r holds the global range shard_range(N, G, r)
+    on devices[r]; init_swarm per shard plus the swarm-wide initial gbest; the
+    speculative passes exchange their records over peer memory (one thread per
+    shard), or -- for shapes without a pass kernel -- every iteration's
+    candidates through the host. compute_seconds = the slowest shard's device
+    time of the iteration loop."""
+    import threading
+    import time
+
+    from .swarm import Swarm, init_shards, p2p_shards, shard_range, step_shards
+    if variant != _lib.SYNC:
+        raise ValueError("exec_options.devices: only cuda-sync shards one swarm over several GPUs")
+    if observe is not None:
+        raise ValueError("exec_options.devices: the per-iteration observer needs a single-device run")
+    G, T = len(devices), p.max_iter
+    parts = []
+    try:
+        for r in range(G):
+            a, c = shard_range(p.particle_cnt, G, r)
+            parts.append(Swarm(p, f, key, device=devices[r], first=a, count=c, init=False))
+        init_shards(parts)
+        try:
+            p2p_shards(parts)
+            fused = True
+        except ValueError:  # no speculative kernel for this shape
+            fused = False
+        secs = [0.0] * G
+        if fused:
+            errs: list[BaseException] = []
+
+            def go(r):
+                try:
+                    secs[r] = parts[r].step(variant, T)
+                except BaseException as e:  # re-raised below
+                    errs.append(e)
+            ths = [threading.Thread(target=go, args=(r,)) for r in range(G)]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            if errs:
+                raise errs[0]
+        else:
+            for sh in parts:
+                sh.synchronize()
+            t0 = time.perf_counter()
+            step_shards(parts, T)
+            for sh in parts:
+                sh.synchronize()
+            secs = [time.perf_counter() - t0]
+        tr, tp, occ = parts[0].trace()
+        gb = parts[0].gbest()
+        init_fit, _ = parts[0].initial_gbest()
+        return run_result(gb.fit, gb.pos, gb.particle, init_fit, tr, max(secs), occ, tp)
+    finally:
+        for sh in parts:
+            sh.close()
 
 
 # ----------------------------------------------------------------- engines

@@ -10,7 +10,7 @@ import io
 import os
 import struct
 from dataclasses import dataclass, field
-from typing import Iterable
+from typing import Iterable, Optional
 
 from .engine import exec_options, find_engine, find_fitness, make_params, rng_key
 
@@ -52,6 +52,7 @@ class bench_config:
     fitness: str = "cubic"
     out_path: str = ""
     device: int = 0
+    devices: Optional[tuple] = None  # cuda-sync sharded over these GPUs (exec_options.devices)
 
     def validate(self) -> None:
         if self.repeat < 3:
@@ -98,7 +99,7 @@ def run_bench(cfg: bench_config) -> list[bench_record]:
     engine = find_engine(cfg.engine)
     f = find_fitness(cfg.fitness)
     p = make_params(f, cfg.particles, cfg.dims, cfg.iters, cfg.group_size)
-    opts = exec_options(device=cfg.device)
+    opts = exec_options(device=cfg.device, devices=cfg.devices)
     csv = None
     if cfg.out_path:
         fresh = not os.path.exists(cfg.out_path)

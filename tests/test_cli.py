@@ -46,3 +46,22 @@ def test_bench_all_engines_table(cupso, tmp_path):
     assert r2.returncode == 0 and "cuda-sync" in r2.stdout
     occ = (tmp_path / "occ.csv").read_text().splitlines()
     assert occ[0] == "iteration,occupancy" and len(occ) == 26
+
+
+def test_devices_shards_cuda_sync_only(cupso):
+    """--devices shards cuda-sync only: another engine is a usage error."""
+    r = cli("--engine", "cuda-queue-lock", "--devices", "2", "--out", "")
+    assert r.returncode == 2
+    assert "--devices shards cuda-sync only" in r.stderr
+
+
+@pytest.mark.gpu
+def test_devices_cli_matches_single_gpu(cupso, tmp_path):
+    """--devices 0,0: two shards (here on one GPU) print the single-GPU checksum."""
+    args = ["--engine", "cuda-sync", "--particles", "20001", "--dims", "8", "--fitness", "sphere",
+            "--iters", "60", "--repeat", "3", "--seed", "5", "--out", ""]
+    one = cli(*args, timeout=600)
+    two = cli(*args, "--devices", "0,0", timeout=600)
+    assert one.returncode == 0 and two.returncode == 0, (one.stderr, two.stderr)
+    pick = lambda out: [ln for ln in out.splitlines() if ln.startswith("cuda-sync")][0].split("checksum=")[1]
+    assert pick(one.stdout) == pick(two.stdout)

@@ -523,3 +523,26 @@ def test_two_process_ipc_shards_equal_single_swarm(cupso, p2p, fitness, n, d, T)
         first, count = cupso.shard_range(n, world, rank)
         assert np.frombuffer(pos, np.float64).tobytes() == np.ascontiguousarray(wpos[:, first:first + count]).tobytes()
         assert stats[0] < T
+
+
+@pytest.mark.parametrize("fit,n,d,T,G", [("sphere", 20001, 8, 60, 2), ("cubic", 70001, 1, 200, 3),
+                                         ("rosenbrock", 3001, 300, 6, 2)])
+def test_exec_options_devices_equal_single(cupso, fit, n, d, T, G):
+    """exec_options(devices=...) shards one cuda-sync swarm over several devices of
+    this process (here G shards on one B200): fused peer-memory exchange for
+    shapes with a pass kernel, host propose/commit otherwise (d = 300); the
+    result is the single-GPU run bit for bit."""
+    import numpy as np
+    f = cupso.find_fitness(fit)
+    p = cupso.make_params(f, n, d, T)
+    e = cupso.find_engine("cuda-sync")
+    one = e.run(p, f, cupso.rng_key(9), cupso.exec_options(device=0))
+    many = e.run(p, f, cupso.rng_key(9), cupso.exec_options(devices=(0,) * G))
+    assert np.array_equal(one.trace.view(np.uint64), many.trace.view(np.uint64))
+    assert np.array_equal(one.trace_particle, many.trace_particle)
+    assert np.array_equal(one.queue_occupancy, many.queue_occupancy)
+    assert one.gbest_particle == many.gbest_particle
+    assert np.array_equal(one.gbest_pos.view(np.uint64), many.gbest_pos.view(np.uint64))
+    assert one.initial_gbest_fit == many.initial_gbest_fit
+    with pytest.raises(ValueError):
+        cupso.find_engine("cuda-async").run(p, f, cupso.rng_key(9), cupso.exec_options(devices=(0, 0)))
