@@ -257,7 +257,8 @@ def run_sharded(p: pso_params, f: fitness_fn, key: rng_key, variant: int, device
     speculative passes exchange their records over peer memory (one thread per
     shard), or -- for shapes without a pass kernel -- every iteration's
     candidates through the host. compute_seconds = the slowest shard's device
-    time of the iteration loop."""
+    time of the iteration loop (fused exchange), or the wall time of the
+    host-exchanged loop."""
     import threading
     import time
 
