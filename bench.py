@@ -30,7 +30,8 @@ strong_cfg5: BASELINE configs[4] as a strong-scaling sub-record on every line:
           kernel on the same swarm at N=1).
 other_workloads: BASELINE configs[2] (cfg3, cuda-async) and configs[3] (cfg4,
           cuda-sync) timed in the same run at N=1, each with its roof and the
-          reduction kernel on the same swarm.
+          reduction kernel on the same swarm; plus the FP32 engine on the cfg2
+          swarm (cfg2_fp32, dtype f32: evidence for that engine, not the headline).
 cpu_baseline: the unmodified reference (oracle/_ref, queue-lock engine, all
           host threads) on a bounded sample of the same workload, rank 0 only.
 Multi-GPU: `--gpus N` without WORLD_SIZE re-launches itself under
@@ -493,13 +494,14 @@ def strong_cfg5_leg(cp, torch, pg, dev, local, world, rank, warmup, steps):
     return rec
 
 
-def workload_leg(cp, torch, dev, local, name, warmup, steps):
+def workload_leg(cp, torch, dev, local, name, warmup, steps, variant=None, with_reduction=True):
     """Another BASELINE workload on the same GPU in the same run (rank 0, N=1):
     its default engine, timed exactly like the headline (device time, L2
     flushed, clocks sampled), its binding roof, and the in-repo reduction kernel
     on the same swarm -- so every configs[] row is measured by the driver's own
     bench run, not only the headline."""
-    fitness, n, d, T, variant, desc = WORKLOADS[name]
+    fitness, n, d, T, default_variant, desc = WORKLOADS[name]
+    variant = variant or default_variant
     job = Job(cp, torch, None, dev, local, 1, 0, fitness, n, d, T, variant, True)
     try:
         clk = ClockSampler(local)
@@ -508,18 +510,20 @@ def workload_leg(cp, torch, dev, local, name, warmup, steps):
         s0, s1 = job.spec_at_start, job.sw.spec_stats()
         roof, launches = roofline_of(job, name, variant, secs, K, clocks, [b - a for a, b in zip(s0, s1)], torch)
         value = n * T * K / secs
-        rsecs, rk = job.run(1, 2, cp.find_engine("cuda-reduction"))
-        red = n * T * rk / rsecs
+        red = None
+        if with_reduction:
+            rsecs, rk = job.run(1, 2, cp.find_engine("cuda-reduction"))
+            red = n * T * rk / rsecs
         keep = ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "mode", "inst_per_particle_update",
                 "pipe_fmaheavy")
         return {"metric": "particle-updates/sec", "value": value, "unit": "particle-updates/s", "steps": K,
-                "ms_per_step": 1e3 * secs / K, "dtype": "f64",
+                "ms_per_step": 1e3 * secs / K, "dtype": "f32" if variant == "cuda-sync-f32" else "f64",
                 "config": {"workload": desc, "fitness": fitness, "particles": n, "dims": d,
                            "iterations_per_step": T, "variant": variant},
                 "roofline": {k: v for k, v in roof.items() if k in keep},
                 "hbm_model_frac": roof["hbm_model"]["frac"], "clocks": clocks, "gpu_launches": launches * K,
-                "reduction_baseline": {"variant": "cuda-reduction", "value": red, "unit": "particle-updates/s",
-                                       "speedup": value / red},
+                "reduction_baseline": None if red is None else {
+                    "variant": "cuda-reduction", "value": red, "unit": "particle-updates/s", "speedup": value / red},
                 "final_gbest_fit": job.sw.gbest().fit}
     finally:
         job.close()
@@ -663,6 +667,11 @@ def main():
                 others[name] = workload_leg(cp, torch, dev, local, name, args.warmup, args.steps)
             except Exception as e:  # reported, never fatal for the headline line
                 others[name] = {"error": str(e)}
+        try:  # the FP32 engine on the headline swarm: reduced precision, not the headline
+            others["cfg2_fp32"] = workload_leg(cp, torch, dev, local, "cfg2", args.warmup, args.steps,
+                                               variant="cuda-sync-f32", with_reduction=False)
+        except Exception as e:
+            others["cfg2_fp32"] = {"error": str(e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

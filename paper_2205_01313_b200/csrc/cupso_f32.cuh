@@ -228,6 +228,116 @@ __device__ __forceinline__ void spec32_finish(const KParams& P, const KState32& 
   spec_decide(P, C, sc, rec_out, 1, t_end, kmax);
 }
 
+// One thread unit of a k_spec32 pass (NP adjacent particles from li); false
+// when the pass already failed at t0. As spec_unit of the FP64 kernels.
+template <int F, int D, int NP>
+__device__ __forceinline__ bool spec32_unit(const KParams& P, const KParams32& Q, const KState32& Si,
+                                            const KState32& So, SpecCtl* sc, uint32_t li, uint32_t t0, uint32_t K,
+                                            bool inplace, float snap_fit, const float (&gp)[D], uint32_t& tstop,
+                                            unsigned long long& bkey, uint32_t& adm) {
+  const uint32_t tl = t0 + K - 1;
+  const size_t ld = P.ld;
+  tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+  uint32_t te = min(t0 + K, tstop);
+  if (te <= t0) return false;
+  const uint32_t g0 = P.base + li;
+  float x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
+  bool ok[NP];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const size_t at = static_cast<size_t>(a) * ld + li;
+    ldv32<NP>(Si.pos + at, x[a]);
+    ldv32<NP>(Si.vel + at, v[a]);
+    ldv32<NP>(Si.pb + at, pb[a]);
+  }
+  ldv32<NP>(Si.pbf + li, pbf);
+#pragma unroll
+  for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
+  uint32_t t = t0;
+  bool bad = false, dirty = false;
+  uint32_t odd_w[D][NP][2];  // words 2/3 of the pair's call, for its odd iteration
+  for (; t < te; ++t) {
+    Fit32<F> acc[NP];
+    // warp-uniform: a fresh call on even iterations (and on a unit's first)
+    const bool fresh = !(t & 1u) || t == t0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        float r1, r2;
+        if (fresh) {
+          uint32_t w0, w1;
+          philox_pair(P, t, g0 + k, a, w0, w1, odd_w[a][k][0], odd_w[a][k][1]);
+          r1 = u24((t & 1u) ? odd_w[a][k][0] : w0);
+          r2 = u24((t & 1u) ? odd_w[a][k][1] : w1);
+        } else {
+          r1 = u24(odd_w[a][k][0]);
+          r2 = u24(odd_w[a][k][1]);
+        }
+        const float xv = x[a][k];
+        float nv = __fmaf_rn(Q.c2 * r2, gp[a] - xv, __fmaf_rn(Q.c1 * r1, pb[a][k] - xv, Q.w * v[a][k]));
+        nv = fminf(fmaxf(nv, Q.min_v), Q.max_v);
+        const float nx = fminf(fmaxf(xv + nv, Q.min_pos), Q.max_pos);
+        v[a][k] = nv;
+        x[a][k] = nx;
+        acc[k].add(nx, a);
+      }
+    }
+    float fv[NP];
+    bool any = false;  // fast path: the snapshot is >= every pbest (see k_spec)
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      fv[k] = acc[k].value();
+      any |= ok[k] && fv[k] > pbf[k];
+    }
+    if (any) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const float f = fv[k];
+        if (!ok[k]) continue;
+        if (f > pbf[k]) {
+          dirty = true;
+          pbf[k] = f;
+#pragma unroll
+          for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
+        }
+        if (f > snap_fit) {
+          if (t < tl) {
+            bad = true;
+          } else {
+            ++adm;
+            const unsigned long long kk = key32(f, g0 + k);
+            bkey = kk > bkey ? kk : bkey;
+          }
+        }
+      }
+      if (bad) {
+        atomicMin(&sc->tmin, t);
+        tstop = t;
+        break;
+      }
+    }
+    if (((t - t0) & 15u) == 15u) {
+      tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
+      te = min(te, tstop);
+    }
+  }
+  if (!bad && t == t0 + K) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const size_t at = static_cast<size_t>(a) * ld + li;
+      stv32<NP>(So.pos + at, x[a]);
+      stv32<NP>(So.vel + at, v[a]);
+    }
+    if (!inplace || dirty) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) stv32<NP>(So.pb + static_cast<size_t>(a) * ld + li, pb[a]);
+      stv32<NP>(So.pbf + li, pbf);
+    }
+  }
+  return true;
+}
+
 template <int F, int D, int NP, int MINB>
 __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParams32 Q, KState32 S0, KState32 S1,
                                                               KCtl C, SpecCtl32* sc32, uint32_t t_end, uint32_t kmax,
@@ -263,107 +373,24 @@ __global__ void __launch_bounds__(kSyncThreads, MINB) k_spec32(KParams P, KParam
   unsigned long long bkey = 0;
   uint32_t adm = 0;
   uint32_t tstop = ld_relaxed_gpu(&sc->tmin);
-  const uint32_t units = (P.n + NP - 1) / NP;
-  const size_t ld = P.ld;
-  for (uint32_t u = blockIdx.x * blockDim.x + tid; u < units; u += gridDim.x * blockDim.x) {
-    tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
-    uint32_t te = min(t0 + K, tstop);
-    if (te <= t0) break;
-    const uint32_t li = NP * u, g0 = P.base + li;
-    float x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
-    bool ok[NP];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const size_t at = static_cast<size_t>(a) * ld + li;
-      ldv32<NP>(Si.pos + at, x[a]);
-      ldv32<NP>(Si.vel + at, v[a]);
-      ldv32<NP>(Si.pb + at, pb[a]);
-    }
-    ldv32<NP>(Si.pbf + li, pbf);
-#pragma unroll
-    for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
-    uint32_t t = t0;
-    bool bad = false, dirty = false;
-    uint32_t odd_w[D][NP][2];  // words 2/3 of the pair's call, for its odd iteration
-    for (; t < te; ++t) {
-      Fit32<F> acc[NP];
-      // warp-uniform: a fresh call on even iterations (and on a unit's first)
-      const bool fresh = !(t & 1u) || t == t0;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          float r1, r2;
-          if (fresh) {
-            uint32_t w0, w1;
-            philox_pair(P, t, g0 + k, a, w0, w1, odd_w[a][k][0], odd_w[a][k][1]);
-            r1 = u24((t & 1u) ? odd_w[a][k][0] : w0);
-            r2 = u24((t & 1u) ? odd_w[a][k][1] : w1);
-          } else {
-            r1 = u24(odd_w[a][k][0]);
-            r2 = u24(odd_w[a][k][1]);
-          }
-          const float xv = x[a][k];
-          float nv = __fmaf_rn(Q.c2 * r2, gp[a] - xv, __fmaf_rn(Q.c1 * r1, pb[a][k] - xv, Q.w * v[a][k]));
-          nv = fminf(fmaxf(nv, Q.min_v), Q.max_v);
-          const float nx = fminf(fmaxf(xv + nv, Q.min_pos), Q.max_pos);
-          v[a][k] = nv;
-          x[a][k] = nx;
-          acc[k].add(nx, a);
-        }
-      }
-      float fv[NP];
-      bool any = false;  // fast path: the snapshot is >= every pbest (see k_spec)
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        fv[k] = acc[k].value();
-        any |= ok[k] && fv[k] > pbf[k];
-      }
-      if (any) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const float f = fv[k];
-          if (!ok[k]) continue;
-          if (f > pbf[k]) {
-            dirty = true;
-            pbf[k] = f;
-#pragma unroll
-            for (int a = 0; a < D; ++a) pb[a][k] = x[a][k];
-          }
-          if (f > snap_fit) {
-            if (t < tl) {
-              bad = true;
-            } else {
-              ++adm;
-              const unsigned long long kk = key32(f, g0 + k);
-              bkey = kk > bkey ? kk : bkey;
-            }
-          }
-        }
-        if (bad) {
-          atomicMin(&sc->tmin, t);
-          tstop = t;
-          break;
-        }
-      }
-      if (((t - t0) & 15u) == 15u) {
-        tstop = min(tstop, ld_relaxed_gpu(&sc->tmin));
-        te = min(te, tstop);
-      }
-    }
-    if (!bad && t == t0 + K) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const size_t at = static_cast<size_t>(a) * ld + li;
-        stv32<NP>(So.pos + at, x[a]);
-        stv32<NP>(So.vel + at, v[a]);
-      }
-      if (!inplace || dirty) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) stv32<NP>(So.pb + static_cast<size_t>(a) * ld + li, pb[a]);
-        stv32<NP>(So.pbf + li, pbf);
-      }
-    }
+  // full rounds of NP-particle units, then -- when the last round would be at
+  // most half full -- one round of NP/2-particle units (as k_spec)
+  const uint32_t nthr = gridDim.x * blockDim.x, gt = blockIdx.x * blockDim.x + tid;
+  uint32_t n_main = P.n;
+  if constexpr (NP >= 2) {
+    const uint32_t rem = P.n % (NP * nthr);
+    if (rem && rem <= (NP / 2) * nthr) n_main = P.n - rem;
+  }
+  const uint32_t units = (n_main + NP - 1) / NP;
+  bool live = true;
+  for (uint32_t u = gt; u < units; u += nthr) {
+    if (!(live = spec32_unit<F, D, NP>(P, Q, Si, So, sc, NP * u, t0, K, inplace, snap_fit, gp, tstop, bkey, adm)))
+      break;
+  }
+  if constexpr (NP >= 2) {
+    const uint32_t li = n_main + (NP / 2) * gt;
+    if (live && li < P.n)
+      spec32_unit<F, D, NP / 2>(P, Q, Si, So, sc, li, t0, K, inplace, snap_fit, gp, tstop, bkey, adm);
   }
   spec32_finish(P, So, C, sc32, s_key, s_adm, s_last, t_end, kmax, rec_out, tl, bkey, adm);
 }
