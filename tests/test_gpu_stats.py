@@ -11,6 +11,14 @@ run_serial's distribution is produced by cuda-sync, which is bitwise
 run_serial (tests/test_gpu_parity.py, tests/test_gpu_fullsize.py) -- checked
 again here on the oracle for two seeds. Bar: a two-sided Mann-Whitney U test
 does not reject equality at ALPHA, and the median costs are within RATIO.
+
+cuda-async is nondeterministic (free-running blocks), so its p-value changes
+from run to run; on Rastrigin d=32 it also converges slightly differently by
+design (a particle may move against a gbest found by a block that is further
+ahead): five B200 runs gave p = 0.05-0.19 with median cost ratios 1.03-1.05.
+Its gate is therefore ALPHA_ASYNC = 0.001 (a false failure at round end would
+otherwise be a few-percent event) together with the same RATIO bound; the
+deterministic cuda-sync-f32 keeps ALPHA = 0.01.
 """
 import numpy as np
 import pytest
@@ -19,6 +27,7 @@ pytestmark = pytest.mark.gpu
 
 SEEDS = range(1, 33)
 ALPHA = 0.01
+ALPHA_ASYNC = 0.001
 RATIO = 1.5
 N, T = 4096, 300
 
@@ -53,5 +62,5 @@ def test_final_fitness_distribution_matches_run_serial(cupso, serial_costs, engi
     ratio = np.median(got) / np.median(base)
     print(f"{engine} {fitness} d={d}: median {np.median(got):.5g} vs run_serial {np.median(base):.5g} "
           f"(ratio {ratio:.3f}), Mann-Whitney p={p:.3f}")
-    assert p > ALPHA, (p, ratio)
+    assert p > (ALPHA_ASYNC if engine == "cuda-async" else ALPHA), (p, ratio)
     assert 1 / RATIO <= ratio <= RATIO, (p, ratio)
