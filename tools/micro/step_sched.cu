@@ -10,14 +10,13 @@
 #include "../../paper_2205_01313_b200/csrc/cupso_device.cuh"
 using namespace cupso;
 
-constexpr int NP = 4;
 
 __device__ __forceinline__ void fence_block(uint32_t t) {
   // a block boundary ptxas cannot schedule across (never taken)
   if (t == 0xfffffff0u) asm volatile("trap;");
 }
 
-template <int V>
+template <int V, int NP = 4>
 __global__ void __launch_bounds__(256, 2) k(KParams P, double* out, uint32_t iters, double g) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t g0 = NP * u;
@@ -93,16 +92,16 @@ __global__ void __launch_bounds__(256, 2) k(KParams P, double* out, uint32_t ite
   out[u] = s;
 }
 
-template <int V>
-void run(const char* name, const KParams& P, double* out, int nsm) {
-  const int grid = 2 * nsm;
+template <int V, int NP = 4>
+void run(const char* name, const KParams& P, double* out, int nsm, int per_sm = 2) {
+  const int grid = per_sm * nsm;
   const uint32_t iters = 4000;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  k<V><<<grid, 256>>>(P, out, 10, 0.5);
+  k<V, NP><<<grid, 256>>>(P, out, 10, 0.5);
   cudaEventRecord(a);
-  k<V><<<grid, 256>>>(P, out, iters, 0.5);
+  k<V, NP><<<grid, 256>>>(P, out, iters, 0.5);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -124,6 +123,11 @@ int main() {
   for (int rep = 0; rep < 2; ++rep) {
     run<0>("V0 straight (k_spec body)", P, out, nsm);
     run<1>("V1 halves, mixed blocks", P, out, nsm);
+    // the tail round's shapes: per-particle rate of NP = 2 at full occupancy,
+    // and of NP = 4 with half / a quarter of the warps
+    run<0, 2>("V0 NP=2, 16 warps/SM", P, out, nsm);
+    run<0, 4>("V0 NP=4, 8 warps/SM", P, out, nsm, 1);
+    run<0, 1>("V0 NP=1, 16 warps/SM", P, out, nsm);
   }
   return 0;
 }
