@@ -174,6 +174,10 @@ struct cupso_swarm {
   KState S_alt{};              // the pass's write buffer (ping-pong with S)
   SpecCtl* spec_ctl = nullptr; // device pass schedule
   SpecCtl* spec_host = nullptr;  // pinned mirror
+  // pinned staging for the per-run read-backs (trace, trace_idx, admitted,
+  // trace_key, gbest record): pageable copies cost ~10 us each
+  unsigned char* pin = nullptr;
+  size_t pin_bytes = 0;
   uint32_t spec_kmax = 64;
   size_t spec_smem = 0;        // dynamic SMEM of the chosen spec kernel
   // host-driven exchange (cupso_step_exchange): the caller's all-gather
@@ -885,6 +889,31 @@ cupso_status create_impl(const cupso_params* p, int fid, uint64_t seed, int devi
   return CUPSO_OK;
 }
 
+__global__ void k_clear_trace(KCtl C, uint32_t T) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    C.admitted[t] = 0;
+    C.trace_key[t] = 0;
+    C.trace[t] = 0.0;
+    C.trace_idx[t] = kNoParticle;
+  }
+}
+
+// The handle's pinned staging area, grown to at least `bytes` (16-byte aligned slices).
+cupso_status pinned(cupso_swarm* h, size_t bytes, unsigned char** out) {
+  if (h->pin_bytes < bytes) {
+    if (h->pin) cudaFreeHost(h->pin);
+    h->pin = nullptr;
+    h->pin_bytes = 0;
+    void* p = nullptr;
+    CK(cudaMallocHost(&p, bytes));
+    h->pin = static_cast<unsigned char*>(p);
+    h->pin_bytes = bytes;
+  }
+  *out = h->pin;
+  return CUPSO_OK;
+}
+size_t align16(size_t x) { return (x + 15) / 16 * 16; }
+
 cupso_status init_impl(cupso_swarm* h) {
   CK(cudaSetDevice(h->device));
   h->f32_active = false;  // a fresh FP64 swarm
@@ -900,10 +929,9 @@ cupso_status init_impl(cupso_swarm* h) {
   k_argmax_blocks<<<nb, 256, 0, h->stream>>>(h->P, h->S.pbf, h->C.aux_fit, h->C.aux_idx);
   k_argmax_final<<<1, 1024, 0, h->stream>>>(h->P, h->S, h->C, nb);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(h->C.admitted, 0, h->T * 8ull, h->stream));
-  CK(cudaMemsetAsync(h->C.trace_key, 0, h->T * 8ull, h->stream));
-  CK(cudaMemsetAsync(h->C.trace, 0, h->T * 8ull, h->stream));
-  CK(cudaMemsetAsync(h->C.trace_idx, 0xff, h->T * 4ull, h->stream));
+  // the per-iteration records, cleared in one launch instead of four memsets
+  k_clear_trace<<<static_cast<int>(std::min<uint64_t>((h->T + 255) / 256, 1024)), 256, 0, h->stream>>>(h->C, h->T);
+  CK(cudaGetLastError());
   if (h->comm) {  // sharded: the initial gbest is the argmax over all shards
     CK(cudaMemcpyAsync(h->rec_local, h->C.snap, h->rec_bytes, cudaMemcpyDeviceToDevice, h->stream));
     const int rc = nccl().allGather(h->rec_local, h->rec_all, h->rec_bytes, /*ncclInt8*/ 0, h->comm,
@@ -913,9 +941,12 @@ cupso_status init_impl(cupso_swarm* h) {
                                       h->rec_bytes);
     CK(cudaGetLastError());
   }
-  Rec r;
-  CK(cudaMemcpyAsync(&r, h->C.snap, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+  unsigned char* pin = nullptr;
+  TRY(pinned(h, align16(sizeof(Rec)), &pin));
+  CK(cudaMemcpyAsync(pin, h->C.snap, sizeof(Rec), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  Rec r;
+  std::memcpy(&r, pin, sizeof r);
   h->initial_fit = r.fit;
   h->initial_particle = r.particle;
   h->t = 0;
@@ -955,13 +986,14 @@ cupso_status download_impl(cupso_swarm* h, double* positions, double* velocities
 
 cupso_status gbest_impl(cupso_swarm* h, double* fit, uint32_t* particle, double* pos) {
   CK(cudaSetDevice(h->device));
-  std::vector<unsigned char> buf(h->rec_bytes);
-  CK(cudaMemcpyAsync(buf.data(), h->C.snap, h->rec_bytes, cudaMemcpyDeviceToHost, h->stream));
+  unsigned char* buf = nullptr;
+  TRY(pinned(h, align16(h->rec_bytes), &buf));
+  CK(cudaMemcpyAsync(buf, h->C.snap, h->rec_bytes, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  const Rec* r = reinterpret_cast<const Rec*>(buf.data());
+  const Rec* r = reinterpret_cast<const Rec*>(buf);
   if (fit) *fit = r->fit;
   if (particle) *particle = r->particle;
-  if (pos) std::memcpy(pos, buf.data() + sizeof(Rec), sizeof(double) * h->P.d);
+  if (pos) std::memcpy(pos, buf + sizeof(Rec), sizeof(double) * h->P.d);
   return CUPSO_OK;
 }
 
@@ -969,23 +1001,40 @@ uint64_t decode_key(unsigned long long k) {
   return (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
 }
 
+// The trace over [first, first+count); with gfit/gpart/gpos also the gbest
+// record, read back under the same synchronisation (cupso_run's result).
 cupso_status trace_impl(cupso_swarm* h, uint32_t first, uint32_t count, double* trace,
-                        uint32_t* trace_particle, double* occupancy) {
+                        uint32_t* trace_particle, double* occupancy, double* gfit = nullptr,
+                        uint32_t* gpart = nullptr, double* gpos = nullptr) {
   if (static_cast<uint64_t>(first) + count > h->t)
     return fail(CUPSO_EINVAL, "trace range [%u, %u) beyond completed iterations (%u)", first,
                 first + count, h->t);
-  if (!count) return CUPSO_OK;
+  if (!count && !(gfit || gpart || gpos)) return CUPSO_OK;
   CK(cudaSetDevice(h->device));
   // the async cummax needs the prefix; fetch [0, first+count)
   const uint32_t end = first + count;
-  std::vector<double> tr(end);
-  std::vector<uint32_t> ti(end);
-  std::vector<unsigned long long> adm(end), tk(end);
-  CK(cudaMemcpyAsync(tr.data(), h->C.trace, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(ti.data(), h->C.trace_idx, end * 4ull, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(adm.data(), h->C.admitted, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(tk.data(), h->C.trace_key, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
+  const size_t o_ti = align16(end * 8ull), o_adm = o_ti + align16(end * 4ull), o_tk = o_adm + align16(end * 8ull);
+  const size_t o_rec = o_tk + align16(end * 8ull);
+  unsigned char* buf = nullptr;
+  TRY(pinned(h, o_rec + align16(h->rec_bytes), &buf));
+  const bool with_gbest = gfit || gpart || gpos;
+  if (with_gbest)
+    CK(cudaMemcpyAsync(buf + o_rec, h->C.snap, h->rec_bytes, cudaMemcpyDeviceToHost, h->stream));
+  double* tr = reinterpret_cast<double*>(buf);
+  uint32_t* ti = reinterpret_cast<uint32_t*>(buf + o_ti);
+  const unsigned long long* adm = reinterpret_cast<const unsigned long long*>(buf + o_adm);
+  const unsigned long long* tk = reinterpret_cast<const unsigned long long*>(buf + o_tk);
+  CK(cudaMemcpyAsync(tr, h->C.trace, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(ti, h->C.trace_idx, end * 4ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(buf + o_adm, h->C.admitted, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(buf + o_tk, h->C.trace_key, end * 8ull, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  if (with_gbest) {
+    const Rec* r = reinterpret_cast<const Rec*>(buf + o_rec);
+    if (gfit) *gfit = r->fit;
+    if (gpart) *gpart = r->particle;
+    if (gpos) std::memcpy(gpos, buf + o_rec + sizeof(Rec), sizeof(double) * h->P.d);
+  }
   double prev = h->initial_fit;
   for (uint32_t t = 0; t < end; ++t) {
     if (h->is_async[t]) {
@@ -1097,6 +1146,7 @@ cupso_status cupso_destroy(cupso_swarm* h) {
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : h->allocs) cudaFree(p);
   if (h->spec_host) cudaFreeHost(h->spec_host);
+  if (h->pin) cudaFreeHost(h->pin);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -1517,10 +1567,9 @@ cupso_status cupso_run(const cupso_params* p, int fid, uint64_t seed, int varian
     }
   }
   out->compute_seconds = total;
-  TRY(gbest_impl(h, &out->gbest_fit, &out->gbest_particle, out->gbest_pos));
   TRY(trace_impl(h, 0, p->max_iter, out->trace, out->trace_particle,
-                 (variant == CUPSO_REDUCTION || variant == CUPSO_UNROLLED) ? nullptr
-                                                                          : out->queue_occupancy));
+                 (variant == CUPSO_REDUCTION || variant == CUPSO_UNROLLED) ? nullptr : out->queue_occupancy,
+                 &out->gbest_fit, &out->gbest_particle, out->gbest_pos));
   out->has_occupancy = !(variant == CUPSO_REDUCTION || variant == CUPSO_UNROLLED);
   return CUPSO_OK;
 }
