@@ -476,7 +476,9 @@ def strong_cfg5_leg(cp, torch, pg, dev, local, world, rank, warmup, steps):
     fitness, n, d, T = STRONG
     job = Job(cp, torch, pg, dev, local, world, rank, fitness, n, d, T, "cuda-sync", True)
     K = max(1, min(steps, STRONG_MAX_STEPS))
-    secs, K = job.run(max(3, min(warmup, 3)), K)
+    clk = ClockSampler(local)
+    secs, K = job.run(max(3, min(warmup, 3)), K, clocks=clk)
+    clocks = clk.summary()
     s0, s1 = job.spec_at_start, job.sw.spec_stats()
     rec = {"metric": "particle-updates/sec", "value": n * T * K / secs, "unit": "particle-updates/s",
            "n_gpus": world, "steps": K, "warmup": 3, "ms_per_step": 1e3 * secs / K, "scaling": "strong",
@@ -484,7 +486,12 @@ def strong_cfg5_leg(cp, torch, pg, dev, local, world, rank, warmup, steps):
                       "iterations_per_step": T, "variant": "cuda-sync", "parallelism": f"dp{world} (particle shards)",
                       "mode": job.sw.sync_mode(), "passes_per_step": (s1[0] - s0[0]) / K,
                       "falsified_per_step": (s1[1] - s0[1]) / K},
-           "final_gbest_fit": job.sw.gbest().fit}
+           "final_gbest_fit": job.sw.gbest().fit, "clocks": clocks}
+    if world == 1:  # binding roof from the exact-schedule capture of this workload (ncu_bench_r02 cfg5)
+        roof, _ = roofline_of(job, "cfg5", "cuda-sync", secs, K, clocks, [b - a for a, b in zip(s0, s1)], torch)
+        keep = ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "pipe_fmaheavy")
+        rec["roofline"] = {k: v for k, v in roof.items() if k in keep}
+        rec["hbm_model_frac"] = roof["hbm_model"]["frac"]
     if world == 1:  # the in-repo reduction kernel on the same 2^28 swarm (~4 s per step)
         rsecs, rk = job.run(1, 2, cp.find_engine("cuda-reduction"))
         red = n * T * rk / rsecs
