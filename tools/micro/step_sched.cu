@@ -29,9 +29,43 @@ __global__ void __launch_bounds__(256, 2) k(KParams P, double* out, uint32_t ite
     pbf[k] = 1e300;
   }
   uint32_t hits = 0;
+  // V2 / V3: iteration t+1's draws computed during iteration t (all warps / odd warps only)
+  const bool ahead = V == 2 || (V == 3 && ((threadIdx.x >> 5) & 1));
+  double n1[NP], n2[NP];
+  if (V >= 2) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      n1[k] = uniform53(P, 0, g0 + k, 0, 0);
+      n2[k] = uniform53(P, 0, g0 + k, 0, 1);
+    }
+  }
   for (uint32_t t = 0; t < iters; ++t) {
     double f[NP];
-    if constexpr (V == 0) {
+    if constexpr (V >= 2) {
+      if (ahead) {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const double r1 = n1[k], r2 = n2[k];
+          n1[k] = uniform53(P, t + 1, g0 + k, 0, 0);
+          n2[k] = uniform53(P, t + 1, g0 + k, 0, 1);
+          v[k] = vel_step53(P, v[k], x[k], pb[k], g, r1, r2);
+          x[k] = pos_step(P, x[k], v[k]);
+          Fit<kCubic> a;
+          a.add_first(x[k]);
+          f[k] = a.value();
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const double r1 = uniform53(P, t, g0 + k, 0, 0), r2 = uniform53(P, t, g0 + k, 0, 1);
+          v[k] = vel_step53(P, v[k], x[k], pb[k], g, r1, r2);
+          x[k] = pos_step(P, x[k], v[k]);
+          Fit<kCubic> a;
+          a.add_first(x[k]);
+          f[k] = a.value();
+        }
+      }
+    } else if constexpr (V == 0) {
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         const double r1 = uniform53(P, t, g0 + k, 0, 0), r2 = uniform53(P, t, g0 + k, 0, 1);
@@ -128,6 +162,8 @@ int main() {
     run<0, 2>("V0 NP=2, 16 warps/SM", P, out, nsm);
     run<0, 4>("V0 NP=4, 8 warps/SM", P, out, nsm, 1);
     run<0, 1>("V0 NP=1, 16 warps/SM", P, out, nsm);
+    run<2>("V2 draw-ahead, all warps", P, out, nsm);
+    run<3>("V3 draw-ahead, odd warps", P, out, nsm);
   }
   return 0;
 }
