@@ -117,3 +117,43 @@ def test_bench_rejects_world_mismatch():
     out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "8", "--dry-run"],
                          capture_output=True, text=True, timeout=120, cwd=root, env=env)
     assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr
+
+
+def test_cpu_baseline_leg_times_the_reference_engines():
+    """cpu_baseline: the reference's queue-lock on all host cores plus
+    its serial engine on one core and its reduction engine on all cores, each on a
+    bounded sample; it needs no GPU."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    leg = bench.cpu_reference_leg("cubic", 4096, 1, 50, max_seconds=0.5)
+    assert leg["value"] > 0 and leg["cores"] >= 1 and leg["kind"] in ("reference", "port")
+    if leg["kind"] == "reference":
+        eng = leg["other_engines"]
+        assert any(k.startswith("serial (1 thread") for k in eng)
+        assert any(k.startswith("reduction (") for k in eng)
+        assert all(v.get("value", 0) > 0 for v in eng.values()), eng
+
+
+@pytest.mark.gpu
+def test_bench_default_line_carries_every_workload(tmp_path):
+    """The default bench line times cfg3 / cfg4 (+ the FP32 engine) next to the
+    headline, each with its reduction baseline and roof (here with short steps)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "2", "--warmup", "3",
+                          "--no-cpu", "--no-strong", "--no-baseline-kernel"], capture_output=True, text=True,
+                         timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["value"] > 0 and line["roofline"]["bound"] == "issue" and line["gpu_launches"] > 0
+    assert 0 < line["roofline"]["pipe_fmaheavy"]["frac"] < 1
+    ow = line["other_workloads"]
+    for name in ("cfg3", "cfg4"):
+        assert ow[name]["value"] > 0 and ow[name]["reduction_baseline"]["speedup"] > 1, ow[name]
+    assert ow["cfg2_fp32"]["dtype"] == "f32" and ow["cfg2_fp32"]["value"] > 0
