@@ -37,3 +37,46 @@ def test_adapter_acceptance_on_gpu(cupso):
     assert r.returncode == 0, r.stdout + r.stderr
     for name in ("cross-engine-equivalence", "per-iteration-oracle", "convergence-1d-cubic", "error-conventions"):
         assert f"PASS: {name}" in r.stdout
+
+
+BENCH = os.path.join(ROOT, "build", "pso_bench_cuda")
+
+
+def test_cpp_bench_frontend_cpu(cupso, tmp_path):
+    """The C++ pso-bench front-end with the CUDA engines (tests/cpp/pso_bench_cuda.cpp):
+    usage errors exit 2 (pso_bench.cpp's contract), psokit's serial engine runs on
+    the host and prints the survey's golden checksum (cubic d=1, N=256, T=100, seed 1),
+    and the table renders from the CSV it wrote."""
+    if not _build_if_possible() or not os.path.exists(BENCH):
+        pytest.skip("reference headers absent and no prebuilt pso_bench_cuda")
+    r = subprocess.run([BENCH, "--engine", "warpspeed"], capture_output=True, text=True)
+    assert r.returncode == 2 and "unknown engine 'warpspeed'" in r.stderr and "cuda-sync" in r.stderr
+    r = subprocess.run([BENCH, "--particles", "0"], capture_output=True, text=True)
+    assert r.returncode == 2
+    csv = tmp_path / "b.csv"
+    r = subprocess.run([BENCH, "--engine", "serial", "--particles", "256", "--iters", "100", "--repeat", "3",
+                        "--out", str(csv)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "checksum=f0812b0e2b07953b" in r.stdout
+    r = subprocess.run([BENCH, "--from-csv", str(csv)], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("| engine |")
+
+
+@pytest.mark.gpu
+def test_cpp_bench_frontend_serial_vs_cuda(cupso, tmp_path):
+    """One C++ run times psokit's serial engine on the host and the CUDA engines on
+    the GPU through the reference's protocol: every deterministic engine prints
+    serial's trace checksum, and the speedup table has a row per CUDA engine."""
+    if not os.path.exists(BENCH) and not _build_if_possible():
+        pytest.skip("no prebuilt pso_bench_cuda (built where /root/reference exists)")
+    r = subprocess.run([BENCH, "--engine", "serial", "--engine", "cuda-sync", "--engine", "cuda-queue-lock",
+                        "--engine", "cuda-reduction", "--engine", "cuda-async", "--particles", "4096", "--iters",
+                        "300", "--repeat", "3", "--seed", "3", "--out", str(tmp_path / "b.csv"), "--table"],
+                       capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stderr
+    sums = {ln.split()[0]: ln.split("checksum=")[1] for ln in r.stdout.splitlines() if "checksum=" in ln}
+    for e in ("cuda-sync", "cuda-queue-lock", "cuda-reduction"):
+        assert sums[e] == sums["serial"], (e, sums)
+    for e in ("cuda-sync", "cuda-queue-lock", "cuda-reduction", "cuda-async"):
+        assert f"| {e} | 4096 | 1 | 300 |" in r.stdout
