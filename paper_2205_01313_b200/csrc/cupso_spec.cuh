@@ -281,7 +281,6 @@ __device__ __forceinline__ bool spec_unit(const KParams& P, const KState& Si, co
   if (te <= t0) return false;        // the pass already failed at t0
   const uint32_t g0 = P.base + li;
   double x[D][NP], v[D][NP], pb[D][NP], pbf[NP];
-  bool ok[NP];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     const size_t at = static_cast<size_t>(a) * ld + li;
@@ -290,8 +289,12 @@ __device__ __forceinline__ bool spec_unit(const KParams& P, const KState& Si, co
     ldv<NP>(Si.pb + at, pb[a]);
   }
   ldv<NP>(Si.pbf + li, pbf);
+  // a slot past the swarm's end (the last unit's padding) gets pbest_fit +inf:
+  // it never improves, so the per-iteration fast-path test needs no validity
+  // mask (the padding's pbest_fit is never read as a particle's)
 #pragma unroll
-  for (int k = 0; k < NP; ++k) ok[k] = k == 0 || li + k < P.n;
+  for (int k = 1; k < NP; ++k)
+    if (li + k >= P.n) pbf[k] = INFINITY;
   uint32_t t = t0;
   bool bad = false;
   bool dirty = false;  // some pbest of this unit changed
@@ -320,13 +323,13 @@ __device__ __forceinline__ bool spec_unit(const KParams& P, const KState& Si, co
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       fv[k] = acc[k].value();
-      any |= ok[k] && fv[k] > pbf[k];
+      any |= fv[k] > pbf[k];
     }
     if (any) {
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         const double f = fv[k];
-        if (!ok[k]) continue;
+        if (k > 0 && li + k >= P.n) continue;  // padding slot
         if (f > pbf[k]) {  // update_pbest (swarm.hpp:100-108)
           dirty = true;
           pbf[k] = f;
